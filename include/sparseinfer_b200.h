@@ -1,0 +1,144 @@
+/*
+ * sparseinfer_b200.h -- C ABI of the B200 4x1-block INT8 SpMM.
+ *
+ * The reference (sparseinfer 0.1.0, /root/reference/pkg) is pure Python +
+ * numba and has no FFI; its operator API is the set of Python functions in
+ * sparseinfer.kernels (kernels/__init__.py:1-40).  Each entry point below is
+ * what that API binds to when it crosses into native code -- the mapping is
+ * given per function as "replaces <file>:<line>".  Plain C types only: host
+ * arrays are the numpy buffers of Sparse4x1Weight / EpilogueProgram, device
+ * pointers are raw CUDA addresses (torch.Tensor.data_ptr()), the stream is a
+ * cudaStream_t passed as void*.  The library never allocates device memory;
+ * the caller owns every buffer (plan image, activations, outputs, workspace).
+ *
+ * Errors: every function returns an si_status (0 = SI_OK).  The text of the
+ * last error on the calling thread is available from si_last_error().  The
+ * Python layer validates shapes and raises the reference's exception types
+ * (ValueError / SparseFormatError) before calling in; a nonzero status
+ * surfaces as RuntimeError.
+ */
+#ifndef SPARSEINFER_B200_H
+#define SPARSEINFER_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SI_ABI_VERSION 1
+
+typedef enum {
+    SI_OK = 0,
+    SI_EINVAL = 1,       /* bad argument / shape mismatch (reference: ValueError) */
+    SI_EFORMAT = 2,      /* malformed 4x1 encoding (reference: SparseFormatError) */
+    SI_ECUDA = 3,        /* CUDA launch / runtime error */
+    SI_EUNSUPPORTED = 4, /* legal input outside what this build implements */
+    SI_ENOSPACE = 5      /* caller buffer too small */
+} si_status;
+
+/* element types, order of tensor.py:27-31 (DType F32, S8, U8, S32) */
+typedef enum { SI_F32 = 0, SI_S8 = 1, SI_U8 = 2, SI_S32 = 3 } si_dtype;
+
+/* epilogue opcodes, epilogue.py:22-29, plus SI_OP_GELU_ERF (extension) */
+typedef enum {
+    SI_OP_REQUANT = 0, SI_OP_LUT = 1, SI_OP_DEQ = 2, SI_OP_GELU = 3,
+    SI_OP_ADD_SIDE = 4, SI_OP_ADD_CHAN = 5, SI_OP_QUANT = 6, SI_OP_DEQ_ACC = 7,
+    SI_OP_GELU_ERF = 8
+} si_op;
+
+/* activation orientation: logical [K, N] (relayout_activation, spmm.py:82)
+ * or token-major [N, K] (relayout_tokens, spmm.py:96).  Neither is relaid
+ * out: the kernels read both directly. */
+typedef enum { SI_ACT_KN = 0, SI_ACT_NK = 1 } si_act_layout;
+
+/* kernel selection; SI_KERNEL_AUTO picks by shape */
+typedef enum {
+    SI_KERNEL_AUTO = 0,
+    SI_KERNEL_GATHER = 1,  /* K1: CUDA-core dp4a gather over 4x1 micro-tiles */
+    SI_KERNEL_TC = 2,      /* K2: tcgen05 kind::i8 tensor-core tiles */
+    SI_KERNEL_REF = 3      /* naive per-element kernel (spmm_ref, spmm.py:401) */
+} si_kernel;
+
+/* Host view of a Sparse4x1Weight (sparse.py:23-41). */
+typedef struct {
+    int32_t rows;          /* padded to 4 */
+    int32_t cols;          /* K */
+    int32_t logical_rows;  /* M */
+    const int32_t *group_ptr; /* [rows/4 + 1] padded block offsets */
+    const int32_t *idx;       /* [group_ptr[rows/4]] column per block */
+    const int8_t *vals;       /* [4 * group_ptr[rows/4]] micro-tiles */
+} si_weight;
+
+/* Host view of an EpilogueProgram (epilogue.py:34-50). */
+typedef struct {
+    int32_t m;                /* channels == logical_rows */
+    const float *scale_in;    /* [m] */
+    int32_t a_zp;
+    int32_t n_ops;
+    const int32_t *ops;       /* [n_ops] */
+    const float *fparams;     /* [n_ops] */
+    const int32_t *iparams;   /* [n_ops * 3] */
+    int32_t n_luts;
+    const uint8_t *luts;      /* [n_luts * 256] */
+    int32_t n_chans;
+    const float *chans;       /* [n_chans * m] */
+    int32_t out_dtype;        /* si_dtype */
+    int32_t n_sides;
+} si_program;
+
+/* ABI version of the loaded library (SI_ABI_VERSION). */
+int32_t si_abi_version(void);
+
+/* Thread-local text of the last failure ("" if none). */
+const char *si_last_error(void);
+
+/* Size in bytes of the plan image for (weight, program, bias).
+ * replaces plan_spmm, spmm.py:160-189 (tiling, compensation, program). */
+int32_t si_plan_image_size(const si_weight *w, const si_program *p, uint64_t *bytes);
+
+/* Build the plan image into host memory (caller copies it to the device
+ * unchanged; it is position independent).  Validates the encoding
+ * (SI_EFORMAT on idx outside [0, K), as decode_sparse, sparse.py:119-120),
+ * packs the GPU tile formats, computes comp[m] (Sparse4x1Weight.row_sums,
+ * sparse.py:51-62) and adj[m] = bias[m] - a_zp*comp[m] (spmm.py:231), and
+ * compiles the epilogue program (LUT / breakpoint-table forms).
+ * bias may be NULL (zeros, spmm.py:179-180). */
+int32_t si_plan_image_build(const si_weight *w, const si_program *p, const int32_t *bias,
+                            void *host_image, uint64_t bytes);
+
+/* Query facts of a built image: the kernel AUTO would choose for n tokens,
+ * whether the compiled epilogue is bit-exact (0 only for GELU feeding an
+ * f32 output or a residual add, where the device tanh/erf is used), etc. */
+typedef struct {
+    int32_t m, k, groups, out_dtype, epi_mode, exact;
+    int64_t nnz_blocks, padded_blocks;
+    uint64_t image_bytes;
+} si_plan_info;
+int32_t si_plan_info_get(const void *host_image, si_plan_info *info);
+
+/* Device workspace the run needs (0 when none). */
+int32_t si_spmm_workspace_size(const void *host_image, int64_t n, int32_t x_layout,
+                               int32_t kernel, uint64_t *bytes);
+
+/* Run the SpMM: out[n, m] = epilogue(sum_k W[m,k] x[k,n] + adj[m]) for
+ * n < N, m < M, stream-ordered on `stream`.
+ * replaces spmm_exec, spmm.py:283-333 (and its kernels _spmm_task_*, :215-280).
+ *   host_image  the host copy of the image (kernel selection reads it)
+ *   dev_image   the same bytes in device memory (16-byte aligned)
+ *   x           device u8 activation, layout x_layout, leading dim ldx (elements)
+ *   sides       device f32 [n_sides, N, M] or NULL when the program has none
+ *   out         device output [N, ldo] of the program's dtype (ldo >= M)
+ *   workspace   device scratch of si_spmm_workspace_size bytes (may be NULL if 0) */
+int32_t si_spmm(const void *host_image, const void *dev_image, const void *x, int32_t x_layout,
+                int64_t ldx, int64_t n, const float *sides, void *out, int64_t ldo,
+                void *workspace, uint64_t workspace_bytes, int32_t kernel, void *stream);
+
+/* Number of kernels si_spmm launches for these arguments (for launch
+ * accounting in bench.py). */
+int32_t si_spmm_launch_count(const void *host_image, int64_t n, int32_t x_layout, int32_t kernel);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPARSEINFER_B200_H */

@@ -1,0 +1,70 @@
+// image.h -- layout of the plan image (host builder <-> device kernels).
+//
+// One position-independent blob per plan: the host builds it
+// (plan.cpp, si_plan_image_build), Python copies it to a CUDA tensor, the
+// kernels read their sections through byte offsets.  Everything the
+// reference's SpmmPlan holds (spmm.py:110-133) is in here: the weight in
+// the GPU tile formats, adj[m] = bias[m] - a_zp*comp[m] (spmm.py:231), the
+// per-channel scale_in and the compiled epilogue program.
+#pragma once
+#include <stdint.h>
+
+#ifndef __CUDACC__
+#define __host__
+#define __device__
+#endif
+
+#define SI_IMG_MAGIC 0x58344953u /* "SI4X" */
+#define SI_IMG_VERSION 2u
+
+// compiled epilogue forms (see plan.cpp: compile_program)
+enum EpiMode : int32_t {
+    EPI_S32 = 0,         // []                     -> s32 acc+adj (spmm.py:280)
+    EPI_DEQ_F32 = 1,     // [DEQ_ACC]              -> f32
+    EPI_REQUANT = 2,     // [REQUANT]              -> 8-bit
+    EPI_REQUANT_LUT = 3, // [REQUANT, int chain]   -> 256-entry composite table
+    EPI_DEQ_TABLE = 4,   // [DEQ_ACC, f32 unary*, QUANT, int chain] -> breakpoint table over f32
+    EPI_GENERIC = 5      // anything else: device interpreter of _run_chain
+};
+
+struct SiImage {
+    uint32_t magic, version;
+    int32_t M, K, rows, groups;
+    int64_t padded_blocks, nnz_blocks, tiles;  // tiles = padded_blocks / 4
+    int32_t out_dtype, a_zp, n_ops, n_luts, n_chans, n_sides;
+    int32_t epi_mode, exact;
+    // single-op fast paths (EPI_REQUANT / first op of EPI_REQUANT_LUT)
+    float q_scale, q_inv;
+    int32_t q_zp, q_lo, q_hi;
+    int32_t n_bp;          // breakpoints in the EPI_DEQ_TABLE table
+    // tensor-core (K2) geometry
+    int32_t tc_mtiles;     // ceil(M / 128)
+    int32_t tc_kpad;       // K rounded up to 128
+    int32_t pad0, pad1;
+    // section offsets in bytes from the image start (16-byte aligned)
+    uint64_t off_tile_ptr;   // int32 [groups+1]        micro-tile offsets per group
+    uint64_t off_tile_w;     // uint4 [tiles]           reference micro-tiles (sparse.py:28-31)
+    uint64_t off_tile_idx;   // int4  [tiles]           the 4 block columns of each tile
+    uint64_t off_adj;        // int32 [M]               bias - a_zp*comp (wrapped)
+    uint64_t off_scale_in;   // f32   [M]
+    uint64_t off_ops;        // int32 [n_ops]
+    uint64_t off_fparams;    // f32   [n_ops]
+    uint64_t off_finv;       // f32   [n_ops]           f32(1/fparam) for the guard-band fast path
+    uint64_t off_iparams;    // int32 [n_ops*3]
+    uint64_t off_luts;       // u8    [n_luts*256]
+    uint64_t off_chans;      // f32   [n_chans*M]
+    uint64_t off_clut;       // u32   [256]             composite table (EPI_REQUANT_LUT)
+    uint64_t off_bp_x;       // f32   [n_bp]            thresholds (EPI_DEQ_TABLE)
+    uint64_t off_bp_v;       // u32   [n_bp+1]          values (bits of the final state)
+    uint64_t off_tc_wt;      // int8  [tc_kpad][tc_mtiles*128]  W^T dense (K2 B/A operand source)
+    uint64_t total_bytes;
+    uint64_t reserved;
+};
+
+static_assert(sizeof(SiImage) % 16 == 0, "image header must stay 16-byte aligned");
+
+template <typename T>
+static inline __host__ __device__ const T *img_sec(const void *img, uint64_t off)
+{
+    return reinterpret_cast<const T *>(reinterpret_cast<const uint8_t *>(img) + off);
+}

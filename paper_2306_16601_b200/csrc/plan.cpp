@@ -1,0 +1,432 @@
+// plan.cpp -- host side of the C ABI: plan-image builder and program compiler.
+//
+// Replaces plan_spmm (spmm.py:160-189) + the device-facing half of
+// build_program (epilogue.py:61-182).  Compiled with -ffp-contract=off so
+// every host evaluation of the epilogue follows the reference's pinned f64
+// expression trees (tensor.py:9-17, epilogue.py:190-249), calling the same
+// glibc tanh/erf the reference's numba code calls.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <cfloat>
+#include <string>
+#include <vector>
+
+#include "../../include/sparseinfer_b200.h"
+#include "image.h"
+#include "si_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+uint64_t align16(uint64_t v) { return (v + 15) & ~uint64_t(15); }
+
+inline int32_t wrap32(int64_t v) { return (int32_t)(uint32_t)(uint64_t)v; }
+
+// ---- host evaluation of the reference's per-element chain ops -------------
+// (_gelu_scalar epilogue.py:190-194; _quant_scalar :197-204; _run_chain :207-249)
+float h_gelu_tanh(float x)
+{
+    double xd = (double)x;
+    double t = 0.7978845608028654 * (xd + 0.044715 * xd * xd * xd);
+    return (float)(0.5 * xd * (1.0 + std::tanh(t)));
+}
+
+float h_gelu_erf(float x)
+{
+    double xd = (double)x;
+    return (float)(0.5 * xd * (1.0 + std::erf(xd * 0.7071067811865476)));
+}
+
+int32_t h_quant(double x, double scale, int32_t zp, int32_t lo, int32_t hi)
+{
+    double q = std::rint(x / scale) + (double)zp;
+    if (q < (double)lo) q = (double)lo;
+    if (q > (double)hi) q = (double)hi;
+    return (int32_t)q;
+}
+
+struct State {
+    int32_t xi = 0;
+    float xf = 0.0f;
+};
+
+// Applies ops[s0:s1) (all per-tensor unary: LUT, DEQ, GELU*, QUANT) to a state.
+void run_unary(const si_program *p, int s0, int s1, State &st)
+{
+    for (int s = s0; s < s1; ++s) {
+        const int32_t *ip = p->iparams + 3 * s;
+        switch (p->ops[s]) {
+        case SI_OP_LUT: {
+            int32_t key = ip[1] == 1 ? st.xi + 128 : st.xi;
+            uint8_t b = p->luts[(int64_t)ip[0] * 256 + key];
+            st.xi = ip[2] == 1 ? (int32_t)(int8_t)b : (int32_t)b;
+            break;
+        }
+        case SI_OP_DEQ: {
+            float t = (float)st.xi - (float)ip[0];
+            st.xf = t * p->fparams[s];
+            break;
+        }
+        case SI_OP_GELU: st.xf = h_gelu_tanh(st.xf); break;
+        case SI_OP_GELU_ERF: st.xf = h_gelu_erf(st.xf); break;
+        case SI_OP_QUANT:
+            st.xi = h_quant((double)st.xf, (double)p->fparams[s], ip[0], ip[1], ip[2]);
+            break;
+        default: break;
+        }
+    }
+}
+
+bool is_unary(int32_t op)
+{
+    return op == SI_OP_LUT || op == SI_OP_DEQ || op == SI_OP_GELU || op == SI_OP_GELU_ERF ||
+           op == SI_OP_QUANT;
+}
+
+// the live value after the program, as the 32-bit word the kernel stores
+uint32_t final_word(const si_program *p, const State &st)
+{
+    if (p->out_dtype == SI_F32) {
+        uint32_t u;
+        std::memcpy(&u, &st.xf, 4);
+        return u;
+    }
+    return (uint32_t)st.xi;
+}
+
+// ---- breakpoint table: x (f32 after DEQ_ACC) -> final word ---------------
+// f32 values in total order via an int64 key.
+int64_t f2key(float x)
+{
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    return (u & 0x80000000u) ? -(int64_t)(u & 0x7fffffffu) : (int64_t)u;
+}
+
+float key2f(int64_t k)
+{
+    uint32_t u = k < 0 ? (0x80000000u | (uint32_t)(-k)) : (uint32_t)k;
+    float x;
+    std::memcpy(&x, &u, 4);
+    return x;
+}
+
+struct BpTable {
+    std::vector<float> x;     // thresholds: smallest x at which the value changes
+    std::vector<uint32_t> v;  // v[i] for x in [x[i-1], x[i])
+};
+
+// f(x) = ops[1:) applied to xf = x.  Scans the whole finite f32 line at a
+// fixed key stride and bisects every interval whose ends differ.  Exact as
+// long as no value is entered and left again inside one stride (4096 ulps),
+// which the program checks it cannot have been by re-evaluating 64 keys on
+// each side of every threshold.
+bool build_breakpoints(const si_program *p, BpTable &t)
+{
+    auto f = [&](int64_t key) {
+        State st;
+        st.xf = key2f(key);
+        run_unary(p, 1, p->n_ops, st);
+        return final_word(p, st);
+    };
+    const int64_t kmin = f2key(-FLT_MAX), kmax = f2key(FLT_MAX);
+    const int64_t stride = 4096;
+    t.x.clear();
+    t.v.clear();
+    int64_t prev_k = kmin;
+    uint32_t prev_v = f(kmin);
+    t.v.push_back(prev_v);
+    for (int64_t k = kmin + stride;; k += stride) {
+        if (k > kmax) k = kmax;
+        uint32_t v = f(k);
+        if (v != prev_v) {
+            // bisect (prev_k, k]: find the smallest key with value != prev_v
+            int64_t lo = prev_k, hi = k;
+            while (hi - lo > 1) {
+                int64_t mid = lo + (hi - lo) / 2;
+                if (f(mid) == prev_v) lo = mid; else hi = mid;
+            }
+            uint32_t vh = f(hi);
+            // the stretch (hi, k] must be constant vh, else a level was skipped
+            for (int64_t q = hi; q <= k; q += (k - hi) / 64 + 1)
+                if (f(q) != vh) return false;
+            t.x.push_back(key2f(hi));
+            t.v.push_back(vh);
+            prev_v = vh;
+            if (vh != v) return false;
+        }
+        prev_k = k;
+        if (k == kmax) break;
+        if (t.x.size() > 4096) return false;
+    }
+    // local re-check around every threshold
+    for (size_t i = 0; i < t.x.size(); ++i) {
+        int64_t k0 = f2key(t.x[i]);
+        for (int64_t d = -64; d < 64; ++d) {
+            int64_t k = k0 + d;
+            if (k < kmin || k > kmax) continue;
+            uint32_t want = d < 0 ? t.v[i] : t.v[i + 1];
+            if (f(k) != want) return false;
+        }
+    }
+    return true;
+}
+
+struct Compiled {
+    int32_t mode = EPI_GENERIC;
+    int32_t exact = 1;
+    float q_scale = 0, q_inv = 0;
+    int32_t q_zp = 0, q_lo = 0, q_hi = 0;
+    std::vector<uint32_t> clut;
+    BpTable bp;
+};
+
+Compiled compile_program(const si_program *p)
+{
+    Compiled c;
+    const int L = p->n_ops;
+    bool has_gelu = false, has_side = false;
+    for (int s = 0; s < L; ++s) {
+        has_gelu |= p->ops[s] == SI_OP_GELU || p->ops[s] == SI_OP_GELU_ERF;
+        has_side |= p->ops[s] == SI_OP_ADD_SIDE || p->ops[s] == SI_OP_ADD_CHAN;
+    }
+    if (L == 0) { c.mode = EPI_S32; return c; }
+    if (L == 1 && p->ops[0] == SI_OP_DEQ_ACC && p->out_dtype == SI_F32) {
+        c.mode = EPI_DEQ_F32;
+        return c;
+    }
+    bool tail_unary = true;
+    for (int s = 1; s < L; ++s) tail_unary &= is_unary(p->ops[s]);
+    if (p->ops[0] == SI_OP_REQUANT) {
+        const int32_t *ip = p->iparams;
+        c.q_scale = p->fparams[0];
+        c.q_inv = (float)(1.0 / (double)p->fparams[0]);
+        c.q_zp = ip[0]; c.q_lo = ip[1]; c.q_hi = ip[2];
+        if (L == 1) { c.mode = EPI_REQUANT; return c; }
+        if (tail_unary && c.q_hi - c.q_lo < 256) {
+            c.mode = EPI_REQUANT_LUT;
+            c.clut.assign(256, 0);
+            for (int32_t q = c.q_lo; q <= c.q_hi; ++q) {
+                State st;
+                st.xi = q;
+                run_unary(p, 1, L, st);
+                c.clut[q - c.q_lo] = final_word(p, st);
+            }
+            return c;
+        }
+    }
+    if (p->ops[0] == SI_OP_DEQ_ACC && tail_unary) {
+        // the f32 chain must end in an integer state for a finite table
+        bool reaches_int = false;
+        for (int s = 1; s < L; ++s) reaches_int |= p->ops[s] == SI_OP_QUANT;
+        if (reaches_int && build_breakpoints(p, c.bp)) {
+            c.mode = EPI_DEQ_TABLE;
+            return c;
+        }
+    }
+    c.mode = EPI_GENERIC;
+    c.exact = has_gelu ? 0 : 1;
+    (void)has_side;
+    return c;
+}
+
+struct Layout {
+    uint64_t off[16];
+    uint64_t total;
+};
+
+}  // namespace
+
+void si_set_error(const std::string &msg) { g_err = msg; }
+
+extern "C" const char *si_last_error(void) { return g_err.c_str(); }
+
+extern "C" int32_t si_abi_version(void) { return SI_ABI_VERSION; }
+
+static int32_t validate(const si_weight *w, const si_program *p)
+{
+    if (!w || !p) { si_set_error("null weight/program"); return SI_EINVAL; }
+    if (w->rows <= 0 || w->rows % 4 || w->cols <= 0 || w->logical_rows <= 0 ||
+        w->logical_rows > w->rows || w->rows - w->logical_rows >= 4) {
+        si_set_error("bad weight geometry");
+        return SI_EINVAL;
+    }
+    if (p->m != w->logical_rows) {
+        si_set_error("program channel count must match weight rows");
+        return SI_EINVAL;
+    }
+    const int32_t G = w->rows / 4;
+    if (w->group_ptr[0] != 0) { si_set_error("group_ptr[0] != 0"); return SI_EFORMAT; }
+    for (int32_t g = 0; g < G; ++g) {
+        int32_t a = w->group_ptr[g], b = w->group_ptr[g + 1];
+        if (b < a || (b - a) % 4) {
+            si_set_error("group_ptr must be non-decreasing multiples of 4");
+            return SI_EFORMAT;
+        }
+    }
+    int64_t T = w->group_ptr[G];
+    for (int64_t t = 0; t < T; ++t)
+        if (w->idx[t] < 0 || w->idx[t] >= w->cols) {
+            si_set_error("column index out of range");
+            return SI_EFORMAT;
+        }
+    for (int s = 0; s < p->n_ops; ++s) {
+        int32_t op = p->ops[s];
+        if (op < 0 || op > SI_OP_GELU_ERF) { si_set_error("unknown opcode"); return SI_EINVAL; }
+        if (op == SI_OP_LUT && (p->iparams[3 * s] < 0 || p->iparams[3 * s] >= p->n_luts)) {
+            si_set_error("lut index out of range");
+            return SI_EINVAL;
+        }
+        if (op == SI_OP_ADD_CHAN && (p->iparams[3 * s] < 0 || p->iparams[3 * s] >= p->n_chans)) {
+            si_set_error("channel vector index out of range");
+            return SI_EINVAL;
+        }
+        if ((op == SI_OP_REQUANT || op == SI_OP_QUANT || op == SI_OP_DEQ) && !(p->fparams[s] > 0)) {
+            si_set_error("quantization scale must be positive");
+            return SI_EINVAL;
+        }
+    }
+    return SI_OK;
+}
+
+static Layout make_layout(const si_weight *w, const si_program *p, const Compiled &c)
+{
+    Layout l{};
+    const int64_t G = w->rows / 4, T = w->group_ptr[G], tiles = T / 4;
+    const int64_t M = w->logical_rows;
+    const int64_t mt = (M + 127) / 128, kp = (w->cols + 127) / 128 * 128;
+    uint64_t cur = align16(sizeof(SiImage));
+    auto put = [&](int i, uint64_t bytes) { l.off[i] = cur; cur = align16(cur + bytes); };
+    put(0, 4 * (G + 1));
+    put(1, 16 * tiles);
+    put(2, 16 * tiles);
+    put(3, 4 * M);
+    put(4, 4 * M);
+    put(5, 4 * (uint64_t)p->n_ops);
+    put(6, 4 * (uint64_t)p->n_ops);
+    put(7, 4 * (uint64_t)p->n_ops);
+    put(8, 12 * (uint64_t)p->n_ops);
+    put(9, 256 * (uint64_t)p->n_luts);
+    put(10, 4 * (uint64_t)p->n_chans * M);
+    put(11, 4 * 256);
+    put(12, 4 * c.bp.x.size());
+    put(13, 4 * (c.bp.v.size() + 1));
+    put(14, (uint64_t)kp * mt * 128);
+    l.total = cur;
+    return l;
+}
+
+extern "C" int32_t si_plan_image_size(const si_weight *w, const si_program *p, uint64_t *bytes)
+{
+    int32_t rc = validate(w, p);
+    if (rc) return rc;
+    Compiled c = compile_program(p);
+    *bytes = make_layout(w, p, c).total;
+    return SI_OK;
+}
+
+extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, const int32_t *bias,
+                                       void *host_image, uint64_t bytes)
+{
+    int32_t rc = validate(w, p);
+    if (rc) return rc;
+    Compiled c = compile_program(p);
+    Layout l = make_layout(w, p, c);
+    if (bytes < l.total) { si_set_error("image buffer too small"); return SI_ENOSPACE; }
+    uint8_t *base = (uint8_t *)host_image;
+    std::memset(base, 0, l.total);
+    SiImage *h = (SiImage *)base;
+    const int32_t G = w->rows / 4;
+    const int64_t T = w->group_ptr[G], tiles = T / 4, M = w->logical_rows, K = w->cols;
+    h->magic = SI_IMG_MAGIC;
+    h->version = SI_IMG_VERSION;
+    h->M = (int32_t)M; h->K = (int32_t)K; h->rows = w->rows; h->groups = G;
+    h->padded_blocks = T; h->tiles = tiles;
+    h->out_dtype = p->out_dtype; h->a_zp = p->a_zp;
+    h->n_ops = p->n_ops; h->n_luts = p->n_luts; h->n_chans = p->n_chans; h->n_sides = p->n_sides;
+    h->epi_mode = c.mode; h->exact = c.exact;
+    h->q_scale = c.q_scale; h->q_inv = c.q_inv; h->q_zp = c.q_zp; h->q_lo = c.q_lo; h->q_hi = c.q_hi;
+    h->n_bp = (int32_t)c.bp.x.size();
+    h->tc_mtiles = (int32_t)((M + 127) / 128);
+    h->tc_kpad = (int32_t)((K + 127) / 128 * 128);
+    uint64_t *offs = &h->off_tile_ptr;
+    for (int i = 0; i < 15; ++i) offs[i] = l.off[i];
+    h->total_bytes = l.total;
+
+    // micro-tiles: reference layout kept verbatim (sparse.py:28-31)
+    int32_t *tp = (int32_t *)(base + h->off_tile_ptr);
+    for (int32_t g = 0; g <= G; ++g) tp[g] = w->group_ptr[g] / 4;
+    std::memcpy(base + h->off_tile_w, w->vals, (size_t)(16 * tiles));
+    std::memcpy(base + h->off_tile_idx, w->idx, (size_t)(4 * T));
+
+    // compensation (sparse.py:51-62) and adj (spmm.py:231), int32 wrap
+    int64_t nnz = 0;
+    int32_t *adj = (int32_t *)(base + h->off_adj);
+    for (int32_t g = 0; g < G; ++g) {
+        int64_t s[4] = {0, 0, 0, 0};
+        for (int64_t q = w->group_ptr[g]; q < w->group_ptr[g + 1]; ++q) {
+            bool any = false;
+            for (int r = 0; r < 4; ++r) {
+                int8_t v = w->vals[(q / 4) * 16 + r * 4 + (q % 4)];
+                s[r] += v;
+                any |= v != 0;
+            }
+            nnz += any;
+        }
+        for (int r = 0; r < 4; ++r) {
+            int64_t m = (int64_t)g * 4 + r;
+            if (m >= M) break;
+            int32_t comp = wrap32(s[r]);
+            int64_t b = bias ? bias[m] : 0;
+            adj[m] = wrap32(b - (int64_t)p->a_zp * (int64_t)comp);
+        }
+    }
+    h->nnz_blocks = nnz;
+
+    std::memcpy(base + h->off_scale_in, p->scale_in, 4 * (size_t)M);
+    if (p->n_ops) {
+        std::memcpy(base + h->off_ops, p->ops, 4 * (size_t)p->n_ops);
+        std::memcpy(base + h->off_fparams, p->fparams, 4 * (size_t)p->n_ops);
+        float *finv = (float *)(base + h->off_finv);
+        for (int s = 0; s < p->n_ops; ++s)
+            finv[s] = p->fparams[s] > 0 ? (float)(1.0 / (double)p->fparams[s]) : 0.0f;
+        std::memcpy(base + h->off_iparams, p->iparams, 12 * (size_t)p->n_ops);
+    }
+    if (p->n_luts) std::memcpy(base + h->off_luts, p->luts, 256 * (size_t)p->n_luts);
+    if (p->n_chans) std::memcpy(base + h->off_chans, p->chans, 4 * (size_t)p->n_chans * M);
+    if (!c.clut.empty()) std::memcpy(base + h->off_clut, c.clut.data(), 4 * 256);
+    if (!c.bp.x.empty()) {
+        std::memcpy(base + h->off_bp_x, c.bp.x.data(), 4 * c.bp.x.size());
+        std::memcpy(base + h->off_bp_v, c.bp.v.data(), 4 * c.bp.v.size());
+    } else if (!c.bp.v.empty()) {
+        std::memcpy(base + h->off_bp_v, c.bp.v.data(), 4 * c.bp.v.size());
+    }
+
+    // K2 source: dense W^T [kpad][mtiles*128] int8, m contiguous
+    int8_t *wt = (int8_t *)(base + h->off_tc_wt);
+    const int64_t ldm = (int64_t)h->tc_mtiles * 128;
+    for (int32_t g = 0; g < G; ++g)
+        for (int64_t q = w->group_ptr[g]; q < w->group_ptr[g + 1]; ++q)
+            for (int r = 0; r < 4; ++r) {
+                int64_t m = (int64_t)g * 4 + r;
+                int8_t v = w->vals[(q / 4) * 16 + r * 4 + (q % 4)];
+                if (m < M && v) wt[(int64_t)w->idx[q] * ldm + m] += v;
+            }
+    return SI_OK;
+}
+
+extern "C" int32_t si_plan_info_get(const void *host_image, si_plan_info *info)
+{
+    const SiImage *h = (const SiImage *)host_image;
+    if (!h || h->magic != SI_IMG_MAGIC || h->version != SI_IMG_VERSION) {
+        si_set_error("not a plan image");
+        return SI_EINVAL;
+    }
+    info->m = h->M; info->k = h->K; info->groups = h->groups; info->out_dtype = h->out_dtype;
+    info->epi_mode = h->epi_mode; info->exact = h->exact;
+    info->nnz_blocks = h->nnz_blocks; info->padded_blocks = h->padded_blocks;
+    info->image_bytes = h->total_bytes;
+    return SI_OK;
+}

@@ -1,0 +1,198 @@
+"""GPU parity: the product's CUDA path against the reference's outputs.
+
+Bar (BASELINE north_star): bit-exact on s32 accumulators and 8-bit
+outputs; f32 outputs bit-exact except where the program evaluates GELU into
+an f32 value (device tanh/erf), where the tolerance is 1e-5 relative.
+Every call goes through the C ABI (libsparseinfer_b200.so)."""
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import baseline_inputs, digest, golden_case, has_gelu
+from oracle import oracle
+import paper_2306_16601_b200 as P
+from paper_2306_16601_b200 import kernels as K, workloads
+
+pytestmark = pytest.mark.gpu
+F32_RTOL = 1e-5  # north_star tolerance for fp32 dequantized outputs (GELU-in-f32 only)
+
+KERNELS = ["gather", "ref"]
+
+
+def tc_available():
+    from paper_2306_16601_b200 import _lib
+    import ctypes
+    sw = P.encode_sparse(P.generate_pattern_weight(128, 128, 0.5, 0))
+    plan = K.plan_spmm(sw, 1024)
+    b = ctypes.c_uint64(0)
+    return _lib.lib().si_spmm_workspace_size(_lib.ptr(plan.image), 1024, 0, 2, ctypes.byref(b)) == 0 \
+        and plan.info is not None
+
+
+def check_equal(got: np.ndarray, want: np.ndarray, prog, ctx):
+    assert got.shape == want.shape and got.dtype == want.dtype, ctx
+    if want.dtype == np.float32 and has_gelu(prog):
+        np.testing.assert_allclose(got, want, rtol=F32_RTOL, atol=0, err_msg=str(ctx))
+    else:
+        if not np.array_equal(got, want):
+            bad = np.argwhere(got != want)
+            raise AssertionError(f"{ctx}: {len(bad)} mismatches, first {bad[:5].tolist()} "
+                                 f"got {got[tuple(bad[0])]} want {want[tuple(bad[0])]}")
+
+
+def run(sw, x, prog, bias, side=None, kernel="auto", layout="kn", n=None):
+    n = x.shape[1] if n is None else n
+    plan = K.plan_spmm(sw, n, program=prog, bias=bias)
+    if layout == "kn":
+        act = K.relayout_activation(x)
+    else:
+        act = K.relayout_tokens(np.ascontiguousarray(x.T))
+    out = K.spmm_exec(plan, act, sides=side, kernel=kernel)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("layout", ["kn", "nk"])
+def test_golden_cases(golden, kernel, layout):
+    d, meta = golden
+    for i in range(len(meta)):
+        c = golden_case(d, meta, i)
+        got = run(c.sw, c.x, c.prog, c.bias, c.side, kernel, layout)
+        check_equal(got, c.ref, c.prog, (i, c.meta, kernel, layout))
+
+
+def test_extreme_values(golden):
+    d, _ = golden
+    sw = P.encode_sparse(d["extreme_w"], np.full(8, 1e-3, np.float32))
+    for kernel in KERNELS:
+        got = run(sw, d["extreme_x"], K.raw_program(sw), d["extreme_bias"], kernel=kernel)
+        assert np.array_equal(got, d["extreme_ref"]), kernel
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_config1_pins(pins, kernel):
+    w, x, bias, scales = baseline_inputs(768, 768, 128, 0.9, 11)
+    sw = P.encode_sparse(w, scales)
+    for kind, key in (("s32", "s32"), ("deq_f32", "f32")):
+        got = run(sw, x, workloads.program(kind, scales), bias, kernel=kernel)
+        assert digest(got) == pins["config1"][key], (kind, kernel)
+
+
+def test_config3_tanh_slice_pin(pins):
+    w, x, bias, scales = baseline_inputs(3072, 768, 4096, 0.8, 13)
+    sw = P.encode_sparse(w, scales)
+    xs = np.ascontiguousarray(x[:, :256])
+    got = run(sw, xs, workloads.program("gelu_tanh_u8", scales), bias)
+    assert digest(got) == pins["config3_slice256"]["u8_tanh"]
+
+
+@pytest.mark.parametrize("kind", ["gelu_erf_u8", "gelu_tanh_u8"])
+def test_config3_full(kind):
+    c = workloads.CONFIG3
+    w, x, bias, scales = baseline_inputs(c.m, c.k, c.n, c.ratio, c.seed)
+    sw = P.encode_sparse(w, scales)
+    prog = workloads.program(kind, scales)
+    want = oracle.spmm_exec(sw, x, prog, bias)
+    got = run(sw, x, prog, bias)
+    check_equal(got, want, prog, kind)
+
+
+@pytest.mark.parametrize("cell", workloads.CONFIG5, ids=lambda c: c.name)
+def test_config5_full_n_against_oracle_slices(cell):
+    """Full N=65536 on the GPU; oracle on three 384-token slices of it."""
+    w, x, bias, scales = baseline_inputs(cell.m, cell.k, cell.n, cell.ratio, cell.seed)
+    sw = P.encode_sparse(w, scales)
+    prog = workloads.program(cell.program, scales)
+    got = run(sw, x, prog, bias)
+    assert got.shape == (cell.n, cell.m)
+    for s0 in (0, 31744, cell.n - 384):
+        xs = np.ascontiguousarray(x[:, s0: s0 + 384])
+        want = oracle.spmm_exec(sw, xs, prog, bias)
+        check_equal(got[s0: s0 + 384], want, prog, (cell.name, s0))
+    # the u8 outputs must be mostly interior (the requant params are meaningful)
+    interior = np.mean((got > 0) & (got < 255))
+    assert interior > 0.9
+
+
+@pytest.mark.parametrize("m,k,n,ratio", [(1, 1, 1, 0.0), (7, 63, 50, 0.5), (130, 257, 1029, 0.85),
+                                         (256, 64, 4097, 0.7), (4, 4096, 33, 0.9), (1000, 300, 2000, 1.0),
+                                         (64, 200, 300, 0.0)])
+@pytest.mark.parametrize("kind", ["s32", "deq_f32", "requant_u8", "gelu_erf_u8"])
+def test_shapes_against_oracle(m, k, n, ratio, kind):
+    w, x, bias, scales = baseline_inputs(m, k, n, ratio, 1234 + m + k)
+    sw = P.encode_sparse(w, scales)
+    prog = workloads.program(kind, scales, a_zp=3)
+    want = oracle.spmm_exec(sw, x, prog, bias)
+    for kernel in KERNELS:
+        for layout in ("kn", "nk"):
+            check_equal(run(sw, x, prog, bias, kernel=kernel, layout=layout), want, prog,
+                        (m, k, n, ratio, kind, kernel, layout))
+
+
+def test_requant_guard_band_exhaustive_boundaries():
+    """Accumulators that land exactly on / next to half-integers after
+    requantization: the f32 fast path must hand them to the f64 path."""
+    m, k = 4, 1
+    w = np.ones((m, k), np.int8)
+    sw = P.encode_sparse(w, np.ones(m, np.float32))
+    for scale, zp in ((2.0, 128), (0.5, 3), (3.0, 100), (1.0 / 3.0, 0)):
+        prog = K.build_program(np.array([1.0, 0.25, 0.1, 7.0], np.float32), 1.0, 0,
+                               P.QuantParams(np.float32(scale), zp, P.DType.U8))
+        # x in [0,255] -> acc = x + bias; sweep bias so acc covers a wide range
+        for b0 in range(-3000, 3000, 251):
+            bias = np.array([b0, b0 * 3, b0 * 7, b0 // 5], np.int32)
+            x = np.arange(256, dtype=np.uint8).reshape(1, 256)
+            want = oracle.spmm_ref(sw, x, prog, bias)
+            got = run(sw, x, prog, bias)
+            assert np.array_equal(got, want), (scale, zp, b0)
+
+
+def test_fault_injection_detected():
+    """flip one stored weight byte -> parity must fail."""
+    w, x, bias, scales = baseline_inputs(256, 256, 512, 0.8, 77)
+    sw = P.encode_sparse(w, scales)
+    prog = workloads.program("requant_u8", scales)
+    plan = K.plan_spmm(sw, 512, program=prog, bias=bias)
+    want = oracle.spmm_exec(sw, x, prog, bias)
+    act = K.relayout_activation(x)
+    ok = K.spmm_exec(plan, act).cpu().numpy()
+    assert np.array_equal(ok, want)
+    hdr = plan.image[:256].view(np.uint64)
+    off_w = int(hdr[16])
+    # first nonzero weight byte of the first tile
+    tile = plan.image[off_w: off_w + 16].view(np.int8)
+    j = int(np.flatnonzero(tile)[0])
+    plan.image_dev[off_w + j] = int(np.uint8(plan.image[off_w + j]) ^ 0x40)
+    bad = K.spmm_exec(plan, act).cpu().numpy()
+    assert not np.array_equal(bad, want)
+
+
+def test_spmm_ref_device_matches_exec(golden):
+    d, meta = golden
+    for i in range(0, len(meta), 5):
+        c = golden_case(d, meta, i)
+        got = K.spmm_ref(c.sw, c.x, c.prog, c.bias, c.side).cpu().numpy()
+        check_equal(got, c.ref, c.prog, i)
+
+
+def test_validation_errors():
+    w, x, bias, scales = baseline_inputs(16, 32, 64, 0.5, 1)
+    sw = P.encode_sparse(w, scales)
+    plan = K.plan_spmm(sw, 64)
+    with pytest.raises(ValueError):
+        K.spmm_exec(plan, K.relayout_activation(x[:, :32]))
+    with pytest.raises(ValueError):
+        K.plan_spmm(sw, 0)
+    with pytest.raises(ValueError):
+        K.plan_spmm(sw, 64, bn=24)
+    with pytest.raises(ValueError):
+        K.plan_spmm(sw, 64, bias=np.zeros(3, np.int32))
+    prog = K.build_program(scales, 1.0, 0, None, [("dequantize_acc",), ("add_side", 0)])
+    plan = K.plan_spmm(sw, 64, program=prog)
+    with pytest.raises(ValueError):
+        K.spmm_exec(plan, K.relayout_activation(x))
+    with pytest.raises(ValueError):
+        K.spmm_exec(plan, K.relayout_activation(x), sides=np.zeros((1, 64, 16), np.float32),
+                    out=torch.empty((64, 16), dtype=torch.int32, device="cuda"))
