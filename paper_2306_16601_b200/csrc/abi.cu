@@ -23,12 +23,13 @@ const SiImage *check_image(const void *host_image)
     return h;
 }
 
-int32_t pick_kernel(const SiImage *h, int64_t n, int32_t layout, int32_t kernel, int64_t ldx, int64_t ldo)
+int32_t pick_kernel(const SiImage *h, int64_t n, int32_t layout, int32_t kernel, const void *x, int64_t ldx,
+                    int64_t ldo)
 {
     if (kernel != SI_KERNEL_AUTO) return kernel;
     // tensor cores once the token tile is worth a 128-row MMA tile; the
     // crossover is measured
-    if (n >= 1024 && k2_supported(h, n, layout, ldx, ldo)) return SI_KERNEL_TC;
+    if (n >= 1024 && k2_supported(h, n, layout, x, ldx, ldo)) return SI_KERNEL_TC;
     return SI_KERNEL_GATHER;
 }
 
@@ -39,7 +40,7 @@ extern "C" int32_t si_spmm_workspace_size(const void *host_image, int64_t n, int
 {
     const SiImage *h = check_image(host_image);
     if (!h) return SI_EINVAL;
-    int32_t k = pick_kernel(h, n, x_layout, kernel, x_layout == SI_ACT_KN ? n : h->K, h->M);
+    int32_t k = pick_kernel(h, n, x_layout, kernel, nullptr, x_layout == SI_ACT_KN ? n : h->K, h->M);
     *bytes = k == SI_KERNEL_GATHER ? k1_workspace(h, n, x_layout)
            : k == SI_KERNEL_TC     ? k2_workspace(h, n, x_layout)
                                    : 0;
@@ -50,7 +51,7 @@ extern "C" int32_t si_spmm_launch_count(const void *host_image, int64_t n, int32
 {
     const SiImage *h = check_image(host_image);
     if (!h) return -1;
-    int32_t k = pick_kernel(h, n, x_layout, kernel, x_layout == SI_ACT_KN ? n : h->K, h->M);
+    int32_t k = pick_kernel(h, n, x_layout, kernel, nullptr, x_layout == SI_ACT_KN ? n : h->K, h->M);
     return k == SI_KERNEL_GATHER ? k1_launch_count(h, x_layout)
          : k == SI_KERNEL_TC     ? k2_launch_count(h, x_layout)
                                  : 1;
@@ -82,7 +83,7 @@ extern "C" int32_t si_spmm(const void *host_image, const void *dev_image, const 
         si_set_error("program needs side inputs");
         return SI_EINVAL;
     }
-    int32_t k = pick_kernel(h, n, x_layout, kernel, ldx, ldo);
+    int32_t k = pick_kernel(h, n, x_layout, kernel, x, ldx, ldo);
     uint64_t need = k == SI_KERNEL_GATHER ? k1_workspace(h, n, x_layout)
                   : k == SI_KERNEL_TC     ? k2_workspace(h, n, x_layout)
                                           : 0;
@@ -90,7 +91,7 @@ extern "C" int32_t si_spmm(const void *host_image, const void *dev_image, const 
         si_set_error("workspace too small: need " + std::to_string(need) + " bytes");
         return SI_ENOSPACE;
     }
-    if (k == SI_KERNEL_TC && !k2_supported(h, n, x_layout, ldx, ldo)) {
+    if (k == SI_KERNEL_TC && !k2_supported(h, n, x_layout, x, ldx, ldo)) {
         si_set_error("tensor-core kernel does not support this shape/layout");
         return SI_EUNSUPPORTED;
     }

@@ -162,7 +162,7 @@ __device__ __forceinline__ uint32_t bp_lookup(float x, const float *bx, const ui
 __device__ __forceinline__ uint32_t f2u(float f) { return __float_as_uint(f); }
 
 // _run_chain interpreter (epilogue.py:207-249) for EPI_GENERIC
-__device__ __noinline__ uint32_t epi_generic(int32_t acc, int32_t m, int64_t n, const EpiParams &E)
+static __device__ __noinline__ uint32_t epi_generic(int32_t acc, int32_t m, int64_t n, const EpiParams &E)
 {
     int32_t xi = 0;
     float xf = 0.0f;

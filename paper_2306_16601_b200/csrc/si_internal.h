@@ -32,6 +32,6 @@ int kref_launch(const SpmmArgs &a);
 
 // K2: tcgen05 tensor-core tiles (spmm_tc.cu)
 int k2_launch(const SpmmArgs &a);
-bool k2_supported(const SiImage *h, int64_t n, int32_t layout, int64_t ldx, int64_t ldo);
+bool k2_supported(const SiImage *h, int64_t n, int32_t layout, const void *x, int64_t ldx, int64_t ldo);
 uint64_t k2_workspace(const SiImage *h, int64_t n, int32_t layout);
 int k2_launch_count(const SiImage *h, int32_t layout);

@@ -1,9 +1,293 @@
-// spmm_tc.cu -- K2, the tcgen05 tensor-core path (work in progress).
+// spmm_tc.cu -- K2: the tensor-core SpMM (tcgen05.mma kind::i8, TMA, TMEM).
+//
+// Replaces the same reference functions as K1 (_acc_group_panel +
+// _spmm_task_*, spmm.py:192-280) for token counts where a 128-row weight
+// tile against a 256-token activation tile is worth a tensor-core pass.
+// The 4x1 blocks are expanded into dense 128 x K weight tiles (W^T, m
+// contiguous, built once by the plan builder); X is read in its native
+// orientation ([K, N] -> MN-major B operand, [N, K] -> K-major B operand),
+// so no relayout pass exists.  Integer MACs are exact and wrap mod 2^32,
+// so the expansion changes no bit of the accumulator.
+//
+// Structure (one persistent CTA per SM, warp-specialised):
+//   warp 0      TMA producer: W^T chunk [128 m x 128 k] and X chunk
+//               [256 n x 128 k] per stage, 4-stage mbarrier ring
+//   warp 1      TMEM allocator + single-thread MMA issuer:
+//               4 x tcgen05.mma.cta_group::1.kind::i8 M128 N256 K32 per stage
+//   warps 2-9   epilogue: tcgen05.ld 32x32b -> registers -> fused epilogue
+//               (epilogue.cuh) -> token-major store out[n, m]
+// TMEM holds two 128 x 256 s32 accumulators (all 512 columns) so the
+// epilogue of tile i overlaps the MMAs of tile i+1.  Tiles are ordered
+// m-fastest so the CTAs working on one token tile run together and share
+// its X chunks through L2.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <stdint.h>
 
+#include <mutex>
+
+#include "epilogue.cuh"
 #include "si_internal.h"
+#include "tc_ptx.cuh"
 
-bool k2_supported(const SiImage *, int64_t, int32_t, int64_t, int64_t) { return false; }
+namespace {
+
+constexpr int BM = 128;     // weight rows per tile (MMA M)
+constexpr int BN = 256;     // tokens per tile (MMA N)
+constexpr int BK = 128;     // k per pipeline stage
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK;           // 16 KB
+constexpr int B_BYTES = BN * BK;           // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 32 * (2 + EPI_WARPS);
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+struct K2Params {
+    int32_t mtiles, ntiles, kchunks;
+    int32_t b_mn_major;  // 1: X is [K, N] (MN-major B), 0: [N, K] (K-major B)
+    int64_t N;
+    void *out;
+    int64_t ldo;
+    int32_t outb;
+};
+
+template <int MODE, int OUTB>
+__global__ void __launch_bounds__(THREADS, 1)
+k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
+             const K2Params P, const EpiParams E)
+{
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t base_u32 = tc::smem_u32(smem_raw);
+    uint8_t *smem = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
+    uint8_t *stage_base = smem;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
+    uint64_t *empty = full + STAGES;
+    uint64_t *tfull = empty + STAGES;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int total_tiles = P.mtiles * P.ntiles;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            tc::mbar_init(&tfull[a], 1);
+            tc::mbar_init(&tempty[a], EPI_WARPS);
+        }
+        tc::mbar_fence_init();
+        tc::tma_prefetch_desc(&tmap_w);
+        tc::tma_prefetch_desc(&tmap_x);
+    }
+    if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+                const int mt = tile % P.mtiles, nt = tile / P.mtiles;
+                for (int kc = 0; kc < P.kchunks; ++kc) {
+                    tc::mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t *a_s = stage_base + stage * STAGE_BYTES;
+                    uint8_t *b_s = a_s + A_BYTES;
+                    tc::mbar_expect_tx(&full[stage], STAGE_BYTES);
+                    tc::tma_load_2d(a_s, &tmap_w, &full[stage], mt * BM, kc * BK);
+                    if (P.b_mn_major) {
+                        tc::tma_load_2d(b_s, &tmap_x, &full[stage], nt * BN, kc * BK);
+                        tc::tma_load_2d(b_s + B_BYTES / 2, &tmap_x, &full[stage], nt * BN + 128, kc * BK);
+                    } else {
+                        tc::tma_load_2d(b_s, &tmap_x, &full[stage], kc * BK, nt * BN);
+                    }
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer (one thread)
+            const uint32_t idesc = tc::idesc_i8(BM, BN, 1, P.b_mn_major ? 1 : 0);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+                tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kc = 0; kc < P.kchunks; ++kc) {
+                    tc::mbar_wait(&full[stage], phase);
+                    tc::tc_fence_after();
+                    const uint32_t a_addr = tc::smem_u32(stage_base + stage * STAGE_BYTES);
+                    const uint32_t b_addr = a_addr + A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < BK / 32; ++kk) {
+                        const uint64_t adesc = tc::smem_desc_sw128(a_addr + kk * 4096, A_BYTES, 1024);
+                        const uint64_t bdesc = P.b_mn_major
+                                                   ? tc::smem_desc_sw128(b_addr + kk * 4096, B_BYTES / 2, 1024)
+                                                   : tc::smem_desc_sw128(b_addr + kk * 32, 16, 1024);
+                        tc::mma_i8(d_tmem, adesc, bdesc, idesc, (kc | kk) ? 1u : 0u);
+                    }
+                    tc::mma_commit(&empty[stage]);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                tc::mma_commit(&tfull[acc]);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+    } else {
+        // ---------------- epilogue warps
+        const int q = warp & 3;             // TMEM lane quarter this warp may access
+        const int h = (warp - 2) >> 2;      // column half
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+            const int mt = tile % P.mtiles, nt = tile / P.mtiles;
+            const int32_t m = mt * BM + q * 32 + lane;
+            const bool mok = m < E.M;
+            const int32_t adj = mok ? __ldg(E.adj + m) : 0;
+            tc::mbar_wait(&tfull[acc], acc_phase);
+            tc::tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < 128 / 32; ++c) {
+                const int col = h * 128 + c * 32;
+                uint32_t r[32];
+                tc::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + col, r);
+                tc::tmem_ld_wait();
+                const int64_t n0 = (int64_t)nt * BN + col;
+                if (mok) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int64_t n = n0 + j;
+                        if (n < P.N) {
+                            const uint32_t v =
+                                epi_apply<MODE>((int32_t)(r[j] + (uint32_t)adj), m, n, E);
+                            if (OUTB == 4)
+                                reinterpret_cast<uint32_t *>(P.out)[n * P.ldo + m] = v;
+                            else
+                                reinterpret_cast<uint8_t *>(P.out)[n * P.ldo + m] = (uint8_t)(v & 0xFF);
+                        }
+                    }
+                }
+            }
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc(tmem_base, 512);
+    }
+}
+
+// ---- host side ------------------------------------------------------------------
+int g_num_sms = 0;
+std::once_flag g_sms_once;
+
+int num_sms()
+{
+    std::call_once(g_sms_once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    });
+    return g_num_sms;
+}
+
+bool encode_2d(CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t outer, uint64_t pitch_bytes,
+               uint32_t box_inner, uint32_t box_outer)
+{
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {pitch_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = cuTensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(ptr), dims, strides,
+                                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int MODE, int OUTB>
+int launch_mode(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx, const K2Params &p)
+{
+    auto kern = k2_tc_kernel<MODE, OUTB>;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        attr_set = true;
+    }
+    EpiParams E = make_epi(a.h, a.img, a.sides, a.n);
+    const int tiles = p.mtiles * p.ntiles;
+    const int grid = tiles < num_sms() ? tiles : num_sms();
+    kern<<<grid, THREADS, SMEM_BYTES, (cudaStream_t)a.stream>>>(tw, tx, p, E);
+    return (int)cudaGetLastError();
+}
+
+template <int OUTB>
+int launch_outb(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx, const K2Params &p)
+{
+    switch (a.h->epi_mode) {
+    case EPI_S32: return launch_mode<EPI_S32, OUTB>(a, tw, tx, p);
+    case EPI_DEQ_F32: return launch_mode<EPI_DEQ_F32, OUTB>(a, tw, tx, p);
+    case EPI_REQUANT: return launch_mode<EPI_REQUANT, OUTB>(a, tw, tx, p);
+    case EPI_REQUANT_LUT: return launch_mode<EPI_REQUANT_LUT, OUTB>(a, tw, tx, p);
+    case EPI_DEQ_TABLE: return launch_mode<EPI_DEQ_TABLE, OUTB>(a, tw, tx, p);
+    default: return launch_mode<EPI_GENERIC, OUTB>(a, tw, tx, p);
+    }
+}
+
+}  // namespace
+
+bool k2_supported(const SiImage *h, int64_t n, int32_t layout, const void *x, int64_t ldx, int64_t)
+{
+    if (n < 1 || n > (int64_t)INT32_MAX - BN) return false;
+    if (((uintptr_t)x) % 16) return false;
+    if (ldx % 16) return false;
+    if (layout == 1 && h->K % 16) return false;  // K-major rows: TMA inner extent granularity
+    return h->tc_mtiles > 0;
+}
+
 uint64_t k2_workspace(const SiImage *, int64_t, int32_t) { return 0; }
+
 int k2_launch_count(const SiImage *, int32_t) { return 1; }
-int k2_launch(const SpmmArgs &) { return (int)cudaErrorNotSupported; }
+
+int k2_launch(const SpmmArgs &a)
+{
+    const SiImage *h = a.h;
+    CUtensorMap tw, tx;
+    const void *wt = img_sec<uint8_t>(a.img, h->off_tc_wt);
+    const uint64_t mpad = (uint64_t)h->tc_mtiles * 128;
+    if (!encode_2d(&tw, wt, mpad, (uint64_t)h->tc_kpad, mpad, 128, BK)) return (int)cudaErrorInvalidValue;
+    bool ok;
+    if (a.layout == 0)
+        ok = encode_2d(&tx, a.x, (uint64_t)a.n, (uint64_t)h->K, (uint64_t)a.ldx, 128, BK);
+    else
+        ok = encode_2d(&tx, a.x, (uint64_t)h->K, (uint64_t)a.n, (uint64_t)a.ldx, BK, BN);
+    if (!ok) return (int)cudaErrorInvalidValue;
+    K2Params p;
+    p.mtiles = h->tc_mtiles;
+    p.ntiles = (int32_t)((a.n + BN - 1) / BN);
+    p.kchunks = h->tc_kpad / BK;
+    p.b_mn_major = a.layout == 0 ? 1 : 0;
+    p.N = a.n;
+    p.out = a.out;
+    p.ldo = a.ldo;
+    p.outb = (h->out_dtype == 0 || h->out_dtype == 3) ? 4 : 1;
+    return p.outb == 4 ? launch_outb<4>(a, tw, tx, p) : launch_outb<1>(a, tw, tx, p);
+}

@@ -48,6 +48,11 @@ def raw_program(sw: Sparse4x1Weight, a_zp: int = 0) -> EpilogueProgram:
     return build_program(sw.scales, 1.0, a_zp, None)
 
 
+def _ld(t: torch.Tensor) -> int:
+    """Row pitch in elements; a single-row tensor may carry any stride(0)."""
+    return int(t.shape[1]) if t.shape[0] == 1 else int(t.stride(0))
+
+
 def _device(device=None) -> torch.device:
     if device is not None:
         return torch.device(device)
@@ -85,7 +90,7 @@ class ActivationLayout:
 
     @property
     def ld(self) -> int:
-        return int(self.data.stride(0))
+        return _ld(self.data)
 
 
 def relayout_activation(a, bn: int = DEFAULT_BN, out=None, device=None) -> ActivationLayout:
@@ -230,7 +235,7 @@ def _run(plan: SpmmPlan, x: torch.Tensor, layout: str, n: int, ldx: int, sides, 
     if out is None:
         out = torch.empty((n, m), dtype=dt, device=dev)
     elif (tuple(out.shape) != (n, m) or out.dtype != dt or not out.is_cuda
-          or out.stride(1) != 1 or out.stride(0) < m):
+          or (m > 1 and out.stride(1) != 1) or _ld(out) < m):
         raise ValueError("bad output buffer")
     lay = _lib.LAYOUTS[layout]
     kid = _lib.KERNELS[kernel]
@@ -240,7 +245,7 @@ def _run(plan: SpmmPlan, x: torch.Tensor, layout: str, n: int, ldx: int, sides, 
     ws = torch.empty(int(ws_bytes.value), dtype=torch.uint8, device=dev) if ws_bytes.value else None
     stream = torch.cuda.current_stream(dev).cuda_stream
     rc = L.si_spmm(img, plan.image_dev.data_ptr(), x.data_ptr(), lay, ldx, n,
-                   sd.data_ptr() if sd is not None else None, out.data_ptr(), out.stride(0),
+                   sd.data_ptr() if sd is not None else None, out.data_ptr(), _ld(out),
                    ws.data_ptr() if ws is not None else None, ws_bytes.value, kid, stream)
     _lib.check(rc, "spmm_exec")
     return out
@@ -268,7 +273,7 @@ def spmm_ref(sw: Sparse4x1Weight, a, program: EpilogueProgram | None = None, bia
     if program is None:
         program = raw_program(sw)
     plan = plan_spmm(sw, int(x.shape[1]), program=program, bias=bias, device=x.device)
-    return _run(plan, x, "kn", int(x.shape[1]), int(x.stride(0)), sides, None, "ref")
+    return _run(plan, x, "kn", int(x.shape[1]), _ld(x), sides, None, "ref")
 
 
 def dot4_accum(a4, b4, acc: int) -> int:
