@@ -58,7 +58,7 @@ struct SiImage {
     uint64_t off_bp_v;       // u32   [n_bp+1]          values (bits of the final state)
     uint64_t off_tc_wt;      // int8  [tc_kpad][tc_mtiles*128]  W^T dense (K2 B/A operand source)
     uint64_t total_bytes;
-    uint64_t reserved;
+    uint64_t off_rqc;        // f32   [M]               f32(f64(scale_in)/f64(fp)) for the requant fast path
 };
 
 static_assert(sizeof(SiImage) % 16 == 0, "image header must stay 16-byte aligned");

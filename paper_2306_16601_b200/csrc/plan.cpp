@@ -233,7 +233,7 @@ Compiled compile_program(const si_program *p)
 }
 
 struct Layout {
-    uint64_t off[16];
+    uint64_t off[17];
     uint64_t total;
 };
 
@@ -314,6 +314,7 @@ static Layout make_layout(const si_weight *w, const si_program *p, const Compile
     put(12, 4 * c.bp.x.size());
     put(13, 4 * (c.bp.v.size() + 1));
     put(14, (uint64_t)kp * mt * 128);
+    put(15, 4 * M);
     l.total = cur;
     return l;
 }
@@ -354,6 +355,7 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
     uint64_t *offs = &h->off_tile_ptr;
     for (int i = 0; i < 15; ++i) offs[i] = l.off[i];
     h->total_bytes = l.total;
+    h->off_rqc = l.off[15];
 
     // micro-tiles: reference layout kept verbatim (sparse.py:28-31)
     int32_t *tp = (int32_t *)(base + h->off_tile_ptr);
@@ -393,6 +395,10 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
         for (int s = 0; s < p->n_ops; ++s)
             finv[s] = p->fparams[s] > 0 ? (float)(1.0 / (double)p->fparams[s]) : 0.0f;
         std::memcpy(base + h->off_iparams, p->iparams, 12 * (size_t)p->n_ops);
+    }
+    if (c.mode == EPI_REQUANT || c.mode == EPI_REQUANT_LUT) {
+        float *rqc = (float *)(base + h->off_rqc);
+        for (int64_t m = 0; m < M; ++m) rqc[m] = (float)((double)p->scale_in[m] / (double)c.q_scale);
     }
     if (p->n_luts) std::memcpy(base + h->off_luts, p->luts, 256 * (size_t)p->n_luts);
     if (p->n_chans) std::memcpy(base + h->off_chans, p->chans, 4 * (size_t)p->n_chans * M);

@@ -14,16 +14,29 @@
 //               [256 n x 128 k] per stage, 4-stage mbarrier ring
 //   warp 1      TMEM allocator + single-thread MMA issuer:
 //               4 x tcgen05.mma.cta_group::1.kind::i8 M128 N256 K32 per stage
-//   warps 2-9   epilogue: tcgen05.ld 32x32b -> registers -> fused epilogue
-//               (epilogue.cuh) -> token-major store out[n, m]
+//   warps 2-9   epilogue: tcgen05.ld 32x32b -> registers -> fused epilogue ->
+//               8-bit outputs: saturating pack, 4x4 quad byte transpose,
+//               128B-swizzled smem tile, TMA store of [128 tokens x 128 m];
+//               32-bit outputs: coalesced 128-byte row stores
 // TMEM holds two 128 x 256 s32 accumulators (all 512 columns) so the
 // epilogue of tile i overlaps the MMAs of tile i+1.  Tiles are ordered
 // m-fastest so the CTAs working on one token tile run together and share
 // its X chunks through L2.
+//
+// Requant fast path (EPI_REQUANT, the BASELINE config-5 epilogue): no
+// conversion instruction (those run on the quarter-rate XU pipe).  The
+// accumulator becomes an f32 by the 1.5*2^23 magic-number trick (exact for
+// |a| < 2^22), r = a * c[m] with c = f32(scale_in/fp), rint(r) by the same
+// magic, and the exactness certificate |r - rint(r)| + 2^-20|r| < 1/2 is
+// max-reduced over each 32-element chunk; a chunk that fails it (or has an
+// out-of-range accumulator) recomputes the flagged elements with the
+// reference's f64 expression (epilogue.py:218-228).  See epilogue.cuh for
+// the error bound.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstring>
 #include <mutex>
 
 #include "epilogue.cuh"
@@ -41,7 +54,12 @@ constexpr int B_BYTES = BN * BK;           // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 32 * (2 + EPI_WARPS);
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int STG_HALF = 128 * 128;        // staging bytes per token half (8-bit outputs)
+constexpr int SMEM_RING = STAGES * STAGE_BYTES;
+constexpr int SMEM_BYTES_8 = SMEM_RING + 2 * STG_HALF + 1024 + 256;
+constexpr int SMEM_BYTES_32 = SMEM_RING + 1024 + 256;
+
+enum OutKind { OUT_32 = 0, OUT_U8_TMA = 1, OUT_S8_TMA = 2, OUT_8_DIRECT = 3 };
 
 struct K2Params {
     int32_t mtiles, ntiles, kchunks;
@@ -49,19 +67,44 @@ struct K2Params {
     int64_t N;
     void *out;
     int64_t ldo;
-    int32_t outb;
+    const float *rqc;    // requant c[m] = f32(scale_in[m] / fp)
 };
 
-template <int MODE, int OUTB>
+constexpr float MAGIC_F = 12582912.0f;     // 1.5 * 2^23
+constexpr int32_t MAGIC_I = 0x4B400000;
+
+__device__ __noinline__ int32_t requant_exact(int32_t a, float s, float fp, int32_t zp, int32_t lo, int32_t hi)
+{
+    double y = __ddiv_rn(__dmul_rn((double)a, (double)s), (double)fp);
+    double q = rint(y) + (double)zp;
+    q = fmin(fmax(q, (double)lo), (double)hi);
+    return (int32_t)q;
+}
+
+__device__ __noinline__ float deq_exact(int32_t a, float s) { return dev_deq_acc(a, s); }
+
+// 4x4 byte transpose inside each quad of lanes: lane 4i+u holds word w = bytes
+// (m = 4i+u; tokens 4w..4w+3) and gets (m = 4i..4i+3; token 4w+u).
+__device__ __forceinline__ uint32_t quad_transpose(uint32_t w, uint32_t selA, uint32_t selB)
+{
+    uint32_t o = __shfl_xor_sync(0xffffffffu, w, 1);
+    uint32_t x = __byte_perm(w, o, selA);
+    uint32_t y = __shfl_xor_sync(0xffffffffu, x, 2);
+    return __byte_perm(x, y, selB);
+}
+
+template <int MODE, int OUTK>
 __global__ void __launch_bounds__(THREADS, 1)
 k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
-             const K2Params P, const EpiParams E)
+             const __grid_constant__ CUtensorMap tmap_o, const K2Params P, const EpiParams E)
 {
+    constexpr bool STAGED = (OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA);
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = tc::smem_u32(smem_raw);
     uint8_t *smem = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
     uint8_t *stage_base = smem;
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
+    uint8_t *staging = smem + SMEM_RING;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + SMEM_RING + (STAGED ? 2 * STG_HALF : 0));
     uint64_t *empty = full + STAGES;
     uint64_t *tfull = empty + STAGES;
     uint64_t *tempty = tfull + 2;
@@ -82,6 +125,7 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
         tc::mbar_fence_init();
         tc::tma_prefetch_desc(&tmap_w);
         tc::tma_prefetch_desc(&tmap_x);
+        if (STAGED) tc::tma_prefetch_desc(&tmap_o);
     }
     if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
     tc::tc_fence_before();
@@ -147,8 +191,13 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
         }
     } else {
         // ---------------- epilogue warps
-        const int q = warp & 3;             // TMEM lane quarter this warp may access
-        const int h = (warp - 2) >> 2;      // column half
+        const int q = warp & 3;             // TMEM lane quarter this warp may access (m sub-block)
+        const int h = (warp - 2) >> 2;      // token half of the 256-token tile
+        const int u = lane & 3, i4 = lane >> 2;
+        const uint32_t selA = (u & 1) ? 0x3715u : 0x6240u;
+        const uint32_t selB = (u & 2) ? 0x3276u : 0x5410u;
+        uint8_t *stg = staging + h * STG_HALF;
+        const bool leader = (q == ((2 + 4 * h) & 3)) && lane == 0;  // first warp of the half
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
@@ -156,6 +205,9 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
             const int32_t m = mt * BM + q * 32 + lane;
             const bool mok = m < E.M;
             const int32_t adj = mok ? __ldg(E.adj + m) : 0;
+            const float s_in = mok ? __ldg(E.scale_in + m) : 0.0f;
+            float cq = 0.0f;
+            if (MODE == EPI_REQUANT) cq = mok ? __ldg(P.rqc + m) : 0.0f;
             tc::mbar_wait(&tfull[acc], acc_phase);
             tc::tc_fence_after();
 #pragma unroll 1
@@ -165,27 +217,117 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
                 tc::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + col, r);
                 tc::tmem_ld_wait();
                 const int64_t n0 = (int64_t)nt * BN + col;
-                if (mok) {
+                int32_t v[32];
+                if constexpr (MODE == EPI_REQUANT) {
+                    const int32_t adjM = (int32_t)((uint32_t)adj + (uint32_t)MAGIC_I);
+                    const int32_t qoff = MAGIC_I - E.q_zp;
+                    float emax = 0.0f;
+                    uint32_t umax = 0;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int32_t b = (int32_t)(r[j] + (uint32_t)adjM);
+                        umax = max(umax, (uint32_t)(b - 0x4B000000));
+                        const float af = __fsub_rn(__int_as_float(b), MAGIC_F);
+                        const float rf = __fmul_rn(af, cq);
+                        const float uu = __fadd_rn(rf, MAGIC_F);
+                        const float d = __fsub_rn(rf, __fsub_rn(uu, MAGIC_F));
+                        emax = fmaxf(emax, __fmaf_rn(fabsf(rf), 9.5367431640625e-07f, fabsf(d)));
+                        v[j] = __float_as_int(uu) - qoff;
+                    }
+                    if (__any_sync(0xffffffffu, emax >= 0.5f || umax >= 0x800000u)) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const int32_t a = (int32_t)(r[j] + (uint32_t)adj);
+                            const int32_t b = (int32_t)((uint32_t)a + (uint32_t)MAGIC_I);
+                            const float rf = __fmul_rn(__fsub_rn(__int_as_float(b), MAGIC_F), cq);
+                            const float d = __fsub_rn(rf, __fsub_rn(__fadd_rn(rf, MAGIC_F), MAGIC_F));
+                            const bool bad = ((uint32_t)(b - 0x4B000000) >= 0x800000u) ||
+                                             !(__fmaf_rn(fabsf(rf), 9.5367431640625e-07f, fabsf(d)) < 0.5f);
+                            if (bad && mok) v[j] = requant_exact(a, s_in, E.q_scale, E.q_zp, E.q_lo, E.q_hi);
+                        }
+                    }
+                    if (OUTK == OUT_32 || OUTK == OUT_8_DIRECT) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] = min(max(v[j], E.q_lo), E.q_hi);
+                    }
+                } else if constexpr (MODE == EPI_S32) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = (int32_t)(r[j] + (uint32_t)adj);
+                } else if constexpr (MODE == EPI_DEQ_F32) {
+                    const int32_t adjM = (int32_t)((uint32_t)adj + (uint32_t)MAGIC_I);
+                    uint32_t umax = 0;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int32_t b = (int32_t)(r[j] + (uint32_t)adjM);
+                        umax = max(umax, (uint32_t)(b - 0x4B000000));
+                        v[j] = __float_as_int(__fmul_rn(__fsub_rn(__int_as_float(b), MAGIC_F), s_in));
+                    }
+                    if (__any_sync(0xffffffffu, umax >= 0x800000u)) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const int32_t a = (int32_t)(r[j] + (uint32_t)adj);
+                            if ((uint32_t)(a + 0x400000) >= 0x800000u) v[j] = __float_as_int(deq_exact(a, s_in));
+                        }
+                    }
+                } else {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         const int64_t n = n0 + j;
-                        if (n < P.N) {
-                            const uint32_t v =
-                                epi_apply<MODE>((int32_t)(r[j] + (uint32_t)adj), m, n, E);
-                            if (OUTB == 4)
-                                reinterpret_cast<uint32_t *>(P.out)[n * P.ldo + m] = v;
-                            else
-                                reinterpret_cast<uint8_t *>(P.out)[n * P.ldo + m] = (uint8_t)(v & 0xFF);
-                        }
+                        v[j] = (mok && n < P.N)
+                                   ? (int32_t)epi_apply<MODE>((int32_t)(r[j] + (uint32_t)adj), m, n, E)
+                                   : 0;
+                    }
+                }
+
+                if constexpr (OUTK == OUT_32) {
+                    if (mok) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (n0 + j < P.N) reinterpret_cast<int32_t *>(P.out)[(n0 + j) * P.ldo + m] = v[j];
+                    }
+                } else if constexpr (OUTK == OUT_8_DIRECT) {
+                    if (mok) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (n0 + j < P.N)
+                                reinterpret_cast<uint8_t *>(P.out)[(n0 + j) * P.ldo + m] = (uint8_t)(v[j] & 0xFF);
+                    }
+                } else {
+                    // saturating pack of 4 consecutive tokens, quad transpose to
+                    // 4 consecutive m, swizzled STS into the [token][128 m] tile
+#pragma unroll
+                    for (int w = 0; w < 8; ++w) {
+                        uint32_t word;
+                        if (OUTK == OUT_U8_TMA)
+                            word = tc::pack_sat_u8(v[4 * w + 1], v[4 * w], tc::pack_sat_u8(v[4 * w + 3], v[4 * w + 2], 0));
+                        else
+                            word = tc::pack_sat_s8(v[4 * w + 1], v[4 * w], tc::pack_sat_s8(v[4 * w + 3], v[4 * w + 2], 0));
+                        word = quad_transpose(word, selA, selB);
+                        const int t = c * 32 + 4 * w + u;                // token row within the half
+                        const int chunk = 2 * q + (i4 >> 2);              // 16B chunk of the 128B row
+                        const int off = t * 128 + (((chunk ^ (t & 7)) << 4)) + 4 * (i4 & 3);
+                        *reinterpret_cast<uint32_t *>(stg + off) = word;
                     }
                 }
             }
+            // this warp's TMEM reads are complete: release the accumulator
             tc::tc_fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+            if constexpr (STAGED) {
+                tc::fence_proxy_async_smem();
+                tc::named_bar_sync(1 + h, 128);
+                if (leader) {
+                    tc::tma_store_2d(&tmap_o, stg, mt * BM, nt * BN + h * 128);
+                    tc::tma_store_commit();
+                    tc::tma_store_wait_read0();
+                }
+                tc::named_bar_sync(1 + h, 128);
+            }
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
+        if (STAGED && leader) tc::tma_store_wait_all0();
     }
     tc::tc_fence_before();
     __syncthreads();
@@ -223,32 +365,35 @@ bool encode_2d(CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t outer, 
     return r == CUDA_SUCCESS;
 }
 
-template <int MODE, int OUTB>
-int launch_mode(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx, const K2Params &p)
+template <int MODE, int OUTK>
+int launch_mode(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx, const CUtensorMap &to,
+                const K2Params &p)
 {
-    auto kern = k2_tc_kernel<MODE, OUTB>;
+    auto kern = k2_tc_kernel<MODE, OUTK>;
+    constexpr int smem = (OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA) ? SMEM_BYTES_8 : SMEM_BYTES_32;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr_set = true;
     }
     EpiParams E = make_epi(a.h, a.img, a.sides, a.n);
     const int tiles = p.mtiles * p.ntiles;
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    kern<<<grid, THREADS, SMEM_BYTES, (cudaStream_t)a.stream>>>(tw, tx, p, E);
+    kern<<<grid, THREADS, smem, (cudaStream_t)a.stream>>>(tw, tx, to, p, E);
     return (int)cudaGetLastError();
 }
 
-template <int OUTB>
-int launch_outb(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx, const K2Params &p)
+template <int OUTK>
+int launch_outk(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx, const CUtensorMap &to,
+                const K2Params &p)
 {
     switch (a.h->epi_mode) {
-    case EPI_S32: return launch_mode<EPI_S32, OUTB>(a, tw, tx, p);
-    case EPI_DEQ_F32: return launch_mode<EPI_DEQ_F32, OUTB>(a, tw, tx, p);
-    case EPI_REQUANT: return launch_mode<EPI_REQUANT, OUTB>(a, tw, tx, p);
-    case EPI_REQUANT_LUT: return launch_mode<EPI_REQUANT_LUT, OUTB>(a, tw, tx, p);
-    case EPI_DEQ_TABLE: return launch_mode<EPI_DEQ_TABLE, OUTB>(a, tw, tx, p);
-    default: return launch_mode<EPI_GENERIC, OUTB>(a, tw, tx, p);
+    case EPI_S32: return launch_mode<EPI_S32, OUTK>(a, tw, tx, to, p);
+    case EPI_DEQ_F32: return launch_mode<EPI_DEQ_F32, OUTK>(a, tw, tx, to, p);
+    case EPI_REQUANT: return launch_mode<EPI_REQUANT, OUTK>(a, tw, tx, to, p);
+    case EPI_REQUANT_LUT: return launch_mode<EPI_REQUANT_LUT, OUTK>(a, tw, tx, to, p);
+    case EPI_DEQ_TABLE: return launch_mode<EPI_DEQ_TABLE, OUTK>(a, tw, tx, to, p);
+    default: return launch_mode<EPI_GENERIC, OUTK>(a, tw, tx, to, p);
     }
 }
 
@@ -270,7 +415,7 @@ int k2_launch_count(const SiImage *, int32_t) { return 1; }
 int k2_launch(const SpmmArgs &a)
 {
     const SiImage *h = a.h;
-    CUtensorMap tw, tx;
+    CUtensorMap tw, tx, to;
     const void *wt = img_sec<uint8_t>(a.img, h->off_tc_wt);
     const uint64_t mpad = (uint64_t)h->tc_mtiles * 128;
     if (!encode_2d(&tw, wt, mpad, (uint64_t)h->tc_kpad, mpad, 128, BK)) return (int)cudaErrorInvalidValue;
@@ -288,6 +433,17 @@ int k2_launch(const SpmmArgs &a)
     p.N = a.n;
     p.out = a.out;
     p.ldo = a.ldo;
-    p.outb = (h->out_dtype == 0 || h->out_dtype == 3) ? 4 : 1;
-    return p.outb == 4 ? launch_outb<4>(a, tw, tx, p) : launch_outb<1>(a, tw, tx, p);
+    p.rqc = img_sec<float>(a.img, h->off_rqc);
+    const bool out32 = h->out_dtype == 0 || h->out_dtype == 3;
+    if (out32) {
+        std::memset(&to, 0, sizeof(to));
+        return launch_outk<OUT_32>(a, tw, tx, to, p);
+    }
+    const bool tma_ok = (a.ldo % 16 == 0) && ((uintptr_t)a.out % 16 == 0) &&
+                        encode_2d(&to, a.out, (uint64_t)h->M, (uint64_t)a.n, (uint64_t)a.ldo, 128, 128);
+    if (!tma_ok) {
+        std::memset(&to, 0, sizeof(to));
+        return launch_outk<OUT_8_DIRECT>(a, tw, tx, to, p);
+    }
+    return h->out_dtype == 2 ? launch_outk<OUT_U8_TMA>(a, tw, tx, to, p) : launch_outk<OUT_S8_TMA>(a, tw, tx, to, p);
 }
