@@ -66,7 +66,7 @@ def build(force: bool = False) -> str:
     with cf.ThreadPoolExecutor(len(SOURCES)) as ex:
         list(ex.map(lambda so: _compile(so[0], so[1], obj_dir), zip(SOURCES, objs)))
     tmp = LIB_PATH + ".tmp"
-    cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-lcuda"]
+    cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")

@@ -40,6 +40,9 @@ struct EpiParams {
     const uint32_t *bp_v;
     const float *sides;   // f32 [n_sides, N, M]
     int64_t N;
+    const int32_t *bp_key;
+    const uint16_t *bp_bucket;
+    int32_t bp_key_lo, bp_shift, bp_nbucket;
 };
 
 static inline EpiParams make_epi(const SiImage *h, const void *img, const float *sides, int64_t n)
@@ -68,6 +71,11 @@ static inline EpiParams make_epi(const SiImage *h, const void *img, const float 
     e.bp_v = img_sec<uint32_t>(img, h->off_bp_v);
     e.sides = sides;
     e.N = n;
+    e.bp_key = img_sec<int32_t>(img, h->off_bp_key);
+    e.bp_bucket = img_sec<uint16_t>(img, h->off_bp_bucket);
+    e.bp_key_lo = h->bp_key_lo;
+    e.bp_shift = h->bp_shift;
+    e.bp_nbucket = h->bp_nbucket;
     return e;
 }
 
@@ -161,6 +169,28 @@ __device__ __forceinline__ uint32_t bp_lookup(float x, const float *bx, const ui
 
 __device__ __forceinline__ uint32_t f2u(float f) { return __float_as_uint(f); }
 
+// f32 -> int32 key preserving the total order of finite floats (+0 == -0)
+__device__ __forceinline__ int32_t f32_key(float x)
+{
+    const uint32_t u = __float_as_uint(x);
+    return (u & 0x80000000u) ? -(int32_t)(u & 0x7fffffffu) : (int32_t)u;
+}
+
+// bucketed breakpoint lookup: value of the piece containing x.  The tables
+// may live in global (read-only path) or shared memory.
+__device__ __forceinline__ uint32_t bp_lookup_bucketed(float x, const int32_t *keys, const uint16_t *bucket,
+                                                       const uint32_t *vals, int n, int32_t key_lo, int shift,
+                                                       int nbucket)
+{
+    const int32_t k = f32_key(x);
+    if (n == 0 || k < key_lo) return vals[0];
+    uint32_t b = ((uint32_t)k - (uint32_t)key_lo) >> shift;
+    b = min(b, (uint32_t)(nbucket - 1));
+    int i = bucket[b];
+    while (i < n && keys[i] <= k) ++i;
+    return vals[i];
+}
+
 // _run_chain interpreter (epilogue.py:207-249) for EPI_GENERIC
 static __device__ __noinline__ uint32_t epi_generic(int32_t acc, int32_t m, int64_t n, const EpiParams &E)
 {
@@ -210,7 +240,8 @@ __device__ __forceinline__ uint32_t epi_apply(int32_t a32, int32_t m, int64_t n,
         return __ldg(E.clut + (q - E.q_lo));
     } else if constexpr (MODE == EPI_DEQ_TABLE) {
         float x = dev_deq_acc(a32, __ldg(E.scale_in + m));
-        return bp_lookup(x, E.bp_x, E.bp_v, E.n_bp);
+        return bp_lookup_bucketed(x, E.bp_key, E.bp_bucket, E.bp_v, E.n_bp, E.bp_key_lo, E.bp_shift,
+                                  E.bp_nbucket);
     } else {
         return epi_generic(a32, m, n, E);
     }

@@ -59,6 +59,10 @@ struct SiImage {
     uint64_t off_tc_wt;      // int8  [tc_kpad][tc_mtiles*128]  W^T dense (K2 B/A operand source)
     uint64_t total_bytes;
     uint64_t off_rqc;        // f32   [M]               f32(f64(scale_in)/f64(fp)) for the requant fast path
+    // bucketed index over the breakpoint thresholds (f32 total-order keys)
+    int32_t bp_key_lo, bp_shift, bp_nbucket, pad2;
+    uint64_t off_bp_key;     // i32   [n_bp]            threshold keys
+    uint64_t off_bp_bucket;  // u16   [bp_nbucket]      first threshold index per key bucket
 };
 
 static_assert(sizeof(SiImage) % 16 == 0, "image header must stay 16-byte aligned");

@@ -181,7 +181,32 @@ struct Compiled {
     int32_t q_zp = 0, q_lo = 0, q_hi = 0;
     std::vector<uint32_t> clut;
     BpTable bp;
+    int32_t bp_key_lo = 0, bp_shift = 0;
+    std::vector<uint16_t> bp_bucket;
 };
+
+// Coarse index over the thresholds in f32 key space: bucket b covers keys
+// [key_lo + (b << shift), key_lo + ((b+1) << shift)); bucket[b] is the number
+// of thresholds with key < bucket start.  A lookup then scans a handful of
+// thresholds instead of a 9-step binary search.
+void build_buckets(Compiled &c)
+{
+    const size_t n = c.bp.x.size();
+    if (n == 0) return;
+    const int64_t lo = f2key(c.bp.x[0]), hi = f2key(c.bp.x[n - 1]);
+    int shift = 0;
+    while (((hi - lo) >> shift) >= 2048) ++shift;
+    const int64_t nb = ((hi - lo) >> shift) + 1;
+    c.bp_key_lo = (int32_t)lo;
+    c.bp_shift = shift;
+    c.bp_bucket.assign((size_t)nb, 0);
+    size_t i = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        const int64_t start = lo + (b << shift);
+        while (i < n && f2key(c.bp.x[i]) < start) ++i;
+        c.bp_bucket[(size_t)b] = (uint16_t)i;
+    }
+}
 
 Compiled compile_program(const si_program *p)
 {
@@ -222,8 +247,14 @@ Compiled compile_program(const si_program *p)
         bool reaches_int = false;
         for (int s = 1; s < L; ++s) reaches_int |= p->ops[s] == SI_OP_QUANT;
         if (reaches_int && build_breakpoints(p, c.bp)) {
-            c.mode = EPI_DEQ_TABLE;
-            return c;
+            build_buckets(c);
+            // keys + values + buckets must fit the kernels' 16 KB smem table
+            if (8 * c.bp.x.size() + 4 + 2 * c.bp_bucket.size() <= 16384) {
+                c.mode = EPI_DEQ_TABLE;
+                return c;
+            }
+            c.bp = BpTable();
+            c.bp_bucket.clear();
         }
     }
     c.mode = EPI_GENERIC;
@@ -233,7 +264,7 @@ Compiled compile_program(const si_program *p)
 }
 
 struct Layout {
-    uint64_t off[17];
+    uint64_t off[18];
     uint64_t total;
 };
 
@@ -315,6 +346,8 @@ static Layout make_layout(const si_weight *w, const si_program *p, const Compile
     put(13, 4 * (c.bp.v.size() + 1));
     put(14, (uint64_t)kp * mt * 128);
     put(15, 4 * M);
+    put(16, 4 * c.bp.x.size());
+    put(17, 2 * c.bp_bucket.size());
     l.total = cur;
     return l;
 }
@@ -356,6 +389,11 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
     for (int i = 0; i < 15; ++i) offs[i] = l.off[i];
     h->total_bytes = l.total;
     h->off_rqc = l.off[15];
+    h->off_bp_key = l.off[16];
+    h->off_bp_bucket = l.off[17];
+    h->bp_key_lo = c.bp_key_lo;
+    h->bp_shift = c.bp_shift;
+    h->bp_nbucket = (int32_t)c.bp_bucket.size();
 
     // micro-tiles: reference layout kept verbatim (sparse.py:28-31)
     int32_t *tp = (int32_t *)(base + h->off_tile_ptr);
@@ -404,6 +442,9 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
     if (p->n_chans) std::memcpy(base + h->off_chans, p->chans, 4 * (size_t)p->n_chans * M);
     if (!c.clut.empty()) std::memcpy(base + h->off_clut, c.clut.data(), 4 * 256);
     if (!c.bp.x.empty()) {
+        int32_t *keys = (int32_t *)(base + h->off_bp_key);
+        for (size_t i = 0; i < c.bp.x.size(); ++i) keys[i] = (int32_t)f2key(c.bp.x[i]);
+        std::memcpy(base + h->off_bp_bucket, c.bp_bucket.data(), 2 * c.bp_bucket.size());
         std::memcpy(base + h->off_bp_x, c.bp.x.data(), 4 * c.bp.x.size());
         std::memcpy(base + h->off_bp_v, c.bp.v.data(), 4 * c.bp.v.size());
     } else if (!c.bp.v.empty()) {

@@ -48,16 +48,24 @@ namespace {
 constexpr int BM = 128;     // weight rows per tile (MMA M)
 constexpr int BN = 256;     // tokens per tile (MMA N)
 constexpr int BK = 128;     // k per pipeline stage
-constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK;           // 16 KB
 constexpr int B_BYTES = BN * BK;           // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 32 * (2 + EPI_WARPS);
 constexpr int STG_HALF = 128 * 128;        // staging bytes per token half (8-bit outputs)
-constexpr int SMEM_RING = STAGES * STAGE_BYTES;
-constexpr int SMEM_BYTES_8 = SMEM_RING + 2 * STG_HALF + 1024 + 256;
-constexpr int SMEM_BYTES_32 = SMEM_RING + 1024 + 256;
+constexpr int TABLE_BYTES = 16 * 1024;    // breakpoint tables staged in smem (EPI_DEQ_TABLE)
+
+// pipeline depth: 4 stages for the fast epilogues, 3 when the epilogue
+// needs shared-memory tables (the L1 carve-out is otherwise ~2 KB)
+template <int MODE>
+constexpr int stages_for() { return (MODE == EPI_DEQ_TABLE || MODE == EPI_REQUANT_LUT || MODE == EPI_GENERIC) ? 3 : 4; }
+template <int MODE, int OUTK>
+constexpr int smem_bytes()
+{
+    return stages_for<MODE>() * STAGE_BYTES + ((OUTK == 1 || OUTK == 2) ? 2 * STG_HALF : 0) +
+           (MODE == EPI_DEQ_TABLE ? TABLE_BYTES : 0) + 1024 + 256;
+}
 
 enum OutKind { OUT_32 = 0, OUT_U8_TMA = 1, OUT_S8_TMA = 2, OUT_8_DIRECT = 3 };
 
@@ -99,12 +107,15 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
              const __grid_constant__ CUtensorMap tmap_o, const K2Params P, const EpiParams E)
 {
     constexpr bool STAGED = (OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA);
+    constexpr int STAGES = stages_for<MODE>();
+    constexpr int SMEM_RING = STAGES * STAGE_BYTES;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = tc::smem_u32(smem_raw);
     uint8_t *smem = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
     uint8_t *stage_base = smem;
     uint8_t *staging = smem + SMEM_RING;
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + SMEM_RING + (STAGED ? 2 * STG_HALF : 0));
+    uint8_t *tables = smem + SMEM_RING + (STAGED ? 2 * STG_HALF : 0);
+    uint64_t *full = reinterpret_cast<uint64_t *>(tables + (MODE == EPI_DEQ_TABLE ? TABLE_BYTES : 0));
     uint64_t *empty = full + STAGES;
     uint64_t *tfull = empty + STAGES;
     uint64_t *tempty = tfull + 2;
@@ -197,6 +208,17 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
         const uint32_t selA = (u & 1) ? 0x3715u : 0x6240u;
         const uint32_t selB = (u & 2) ? 0x3276u : 0x5410u;
         uint8_t *stg = staging + h * STG_HALF;
+        // breakpoint tables -> smem (keys | values | buckets)
+        int32_t *s_key = reinterpret_cast<int32_t *>(tables);
+        uint32_t *s_val = reinterpret_cast<uint32_t *>(tables + 4 * E.n_bp);
+        uint16_t *s_bkt = reinterpret_cast<uint16_t *>(tables + 8 * E.n_bp + 4);
+        if constexpr (MODE == EPI_DEQ_TABLE) {
+            const int et = threadIdx.x - 64;
+            for (int i = et; i < E.n_bp; i += 32 * EPI_WARPS) s_key[i] = __ldg(E.bp_key + i);
+            for (int i = et; i <= E.n_bp; i += 32 * EPI_WARPS) s_val[i] = __ldg(E.bp_v + i);
+            for (int i = et; i < E.bp_nbucket; i += 32 * EPI_WARPS) s_bkt[i] = __ldg(E.bp_bucket + i);
+            tc::named_bar_sync(3, 32 * EPI_WARPS);
+        }
         const bool leader = (q == ((2 + 4 * h) & 3)) && lane == 0;  // first warp of the half
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -268,6 +290,13 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
                             const int32_t a = (int32_t)(r[j] + (uint32_t)adj);
                             if ((uint32_t)(a + 0x400000) >= 0x800000u) v[j] = __float_as_int(deq_exact(a, s_in));
                         }
+                    }
+                } else if constexpr (MODE == EPI_DEQ_TABLE) {
+#pragma unroll 4
+                    for (int j = 0; j < 32; ++j) {
+                        const float x = dev_deq_acc((int32_t)(r[j] + (uint32_t)adj), s_in);
+                        v[j] = (int32_t)bp_lookup_bucketed(x, s_key, s_bkt, s_val, E.n_bp, E.bp_key_lo, E.bp_shift,
+                                                           E.bp_nbucket);
                     }
                 } else {
 #pragma unroll
@@ -352,14 +381,36 @@ int num_sms()
     return g_num_sms;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point, so the
+// library does not link libcuda (it must load on GPU-less build hosts).
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn g_encode = nullptr;
+std::once_flag g_encode_once;
+
+EncodeTiledFn encode_fn()
+{
+    std::call_once(g_encode_once, [] {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_encode = reinterpret_cast<EncodeTiledFn>(fn);
+    });
+    return g_encode;
+}
+
 bool encode_2d(CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t outer, uint64_t pitch_bytes,
                uint32_t box_inner, uint32_t box_outer)
 {
+    EncodeTiledFn enc = encode_fn();
+    if (!enc) return false;
     cuuint64_t dims[2] = {inner, outer};
     cuuint64_t strides[1] = {pitch_bytes};
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = cuTensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(ptr), dims, strides,
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(ptr), dims, strides,
                                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
@@ -370,7 +421,8 @@ int launch_mode(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx,
                 const K2Params &p)
 {
     auto kern = k2_tc_kernel<MODE, OUTK>;
-    constexpr int smem = (OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA) ? SMEM_BYTES_8 : SMEM_BYTES_32;
+    constexpr int smem = smem_bytes<MODE, OUTK>();
+    static_assert(smem <= 232448, "shared memory budget");
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
