@@ -292,7 +292,7 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
                         }
                     }
                 } else if constexpr (MODE == EPI_DEQ_TABLE) {
-#pragma unroll 4
+#pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         const float x = dev_deq_acc((int32_t)(r[j] + (uint32_t)adj), s_in);
                         v[j] = (int32_t)bp_lookup_bucketed(x, s_key, s_bkt, s_val, E.n_bp, E.bp_key_lo, E.bp_shift,
