@@ -1,43 +1,53 @@
 // spmm_tc.cu -- K2: the tensor-core SpMM (tcgen05.mma kind::i8, TMA, TMEM).
 //
 // Replaces the same reference functions as K1 (_acc_group_panel +
-// _spmm_task_*, spmm.py:192-280) for token counts where a 128-row weight
-// tile against a 256-token activation tile is worth a tensor-core pass.
-// The 4x1 blocks are expanded into dense 128 x K weight tiles (W^T, m
+// _spmm_task_*, spmm.py:192-280) for token counts where tensor-core tiles
+// pay.  The 4x1 blocks are expanded into dense weight tiles (W^T, m
 // contiguous, built once by the plan builder); X is read in its native
 // orientation ([K, N] -> MN-major B operand, [N, K] -> K-major B operand),
-// so no relayout pass exists.  Integer MACs are exact and wrap mod 2^32,
-// so the expansion changes no bit of the accumulator.
+// so no relayout pass exists.  Integer MACs are exact and wrap mod 2^32, so
+// the expansion changes no bit of the accumulator.
 //
-// Structure (one persistent CTA per SM, warp-specialised):
-//   warp 0      TMA producer: W^T chunk [128 m x 128 k] and X chunk
-//               [256 n x 128 k] per stage, 4-stage mbarrier ring
-//   warp 1      TMEM allocator + single-thread MMA issuer:
-//               4 x tcgen05.mma.cta_group::1.kind::i8 M128 N256 K32 per stage
-//   warps 2-9   epilogue: tcgen05.ld 32x32b -> registers -> fused epilogue ->
-//               8-bit outputs: saturating pack, 4x4 quad byte transpose,
-//               128B-swizzled smem tile, TMA store of [128 tokens x 128 m];
-//               32-bit outputs: coalesced 128-byte row stores
-// TMEM holds two 128 x 256 s32 accumulators (all 512 columns) so the
-// epilogue of tile i overlaps the MMAs of tile i+1.  Tiles are ordered
-// m-fastest so the CTAs working on one token tile run together and share
-// its X chunks through L2.
+// Two kernels share one epilogue:
 //
-// Requant fast path (EPI_REQUANT, the BASELINE config-5 epilogue): no
-// conversion instruction (those run on the quarter-rate XU pipe).  The
-// accumulator becomes an f32 by the 1.5*2^23 magic-number trick (exact for
-// |a| < 2^22), r = a * c[m] with c = f32(scale_in/fp), rint(r) by the same
-// magic, and the exactness certificate |r - rint(r)| + 2^-20|r| < 1/2 is
-// max-reduced over each 32-element chunk; a chunk that fails it (or has an
-// out-of-range accumulator) recomputes the flagged elements with the
-// reference's f64 expression (epilogue.py:218-228).  See epilogue.cuh for
-// the error bound.
+//  k2p  (default) a CTA *pair* (cluster of 2, tcgen05 cta_group::2).  The
+//       pair computes D[256 W rows x 256 tokens] per MMA tile; each CTA
+//       holds half of A (128 W rows) and half of B (128 tokens) in its smem,
+//       so every SM moves half the operand bytes a single CTA would.  With
+//       K <= 1024 the pair's activation tile stays resident in smem
+//       ("X-stationary") while W streams through the ring, so X is read
+//       from HBM once and only W^T (L2-resident) is re-streamed.
+//  k2   single CTA, M128 x N256 tiles, both operands streamed (kept as the
+//       A/B reference; SI_K2_VARIANT=single selects it).
+//
+// Roles (both kernels): warp 0 TMA producer, warp 1 TMEM allocator + MMA
+// issuer (one thread; in the pair only the leader CTA issues), warps 2..17
+// epilogue (16 warps, 4 per TMEM lane quarter, 64 tokens each).  TMEM holds
+// two 256-column s32 accumulators so the epilogue of tile i overlaps the
+// MMAs of tile i+1.
+//
+// Epilogue (all compiled forms of the reference's _run_chain,
+// epilogue.py:207-249): tcgen05.ld 32x32b.x32 -> registers -> the form's
+// math -> 8-bit outputs: saturating pack, 4x4 quad byte transpose, 128B-
+// swizzled smem tile, TMA store; 32-bit outputs: coalesced 128-byte rows.
+// The requant form (BASELINE config 5) uses no conversion instruction (those
+// run on the quarter-rate XU pipe): the accumulator becomes an f32 by the
+// 1.5*2^23 magic-number trick (exact for |a| < 2^22), r = a * c[m] with
+// c = f32(scale_in/fp) in packed f32x2 ops, rint(r) by the same magic, and
+// the certificate |r - rint(r)| + 2^-20|r| < 1/2 is max-reduced per 32
+// elements; a chunk that fails it (or holds an out-of-range accumulator)
+// recomputes the flagged elements with the reference's f64 expression.
+// Error bound: |r - y| <= 3 * 2^-24 |y| (one rounding each for a, c, a*c;
+// y = the reference's f64 value), so outside the certificate's band rint(r)
+// == rint(y) and the output bits match.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <string>
 
 #include "epilogue.cuh"
 #include "si_internal.h"
@@ -45,37 +55,31 @@
 
 namespace {
 
-constexpr int BM = 128;     // weight rows per tile (MMA M)
-constexpr int BN = 256;     // tokens per tile (MMA N)
-constexpr int BK = 128;     // k per pipeline stage
-constexpr int A_BYTES = BM * BK;           // 16 KB
-constexpr int B_BYTES = BN * BK;           // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int EPI_WARPS = 8;
+constexpr int BK = 128;                     // k per pipeline stage (one 128B swizzle row)
+constexpr int EPI_WARPS = 16;               // 4 per TMEM lane quarter
+constexpr int EPI_GROUPS = EPI_WARPS / 4;   // token column groups
+constexpr int TILE_N = 256;                 // tokens per accumulator tile
+constexpr int COLS = TILE_N / EPI_GROUPS;   // tokens per epilogue warp (64)
 constexpr int THREADS = 32 * (2 + EPI_WARPS);
-constexpr int STG_HALF = 128 * 128;        // staging bytes per token half (8-bit outputs)
-constexpr int TABLE_BYTES = 16 * 1024;    // breakpoint tables staged in smem (EPI_DEQ_TABLE)
-
-// pipeline depth: 4 stages for the fast epilogues, 3 when the epilogue
-// needs shared-memory tables (the L1 carve-out is otherwise ~2 KB)
-template <int MODE>
-constexpr int stages_for() { return (MODE == EPI_DEQ_TABLE || MODE == EPI_REQUANT_LUT || MODE == EPI_GENERIC) ? 3 : 4; }
-template <int MODE, int OUTK>
-constexpr int smem_bytes()
-{
-    return stages_for<MODE>() * STAGE_BYTES + ((OUTK == 1 || OUTK == 2) ? 2 * STG_HALF : 0) +
-           (MODE == EPI_DEQ_TABLE ? TABLE_BYTES : 0) + 1024 + 256;
-}
+constexpr int STG_GROUP = 128 * COLS;       // staging bytes per column group (8-bit outputs)
+constexpr int STG_BYTES = EPI_GROUPS * STG_GROUP;
+constexpr int TABLE_BYTES = 16 * 1024;      // breakpoint tables staged in smem (EPI_DEQ_TABLE)
+constexpr int SMEM_MAX = 232448;
 
 enum OutKind { OUT_32 = 0, OUT_U8_TMA = 1, OUT_S8_TMA = 2, OUT_8_DIRECT = 3 };
 
 struct K2Params {
-    int32_t mtiles, ntiles, kchunks;
+    int32_t mtiles;      // weight-row tiles (128 rows single-CTA, 256 rows per pair)
+    int32_t ntiles;      // 256-token tiles
+    int32_t kchunks;     // K / 128
     int32_t b_mn_major;  // 1: X is [K, N] (MN-major B), 0: [N, K] (K-major B)
+    int32_t mgroups;     // pair X-stationary: m-tiles split into this many work units per token tile
     int64_t N;
     void *out;
     int64_t ldo;
     const float *rqc;    // requant c[m] = f32(scale_in[m] / fp)
+    int32_t debug;       // experiment switches (SI_K2_DEBUG): 1 skip epilogue, 2 W tile 0 only,
+                         // 4 X tile 0 only, 8 no TMA, 16 no MMA
 };
 
 constexpr float MAGIC_F = 12582912.0f;     // 1.5 * 2^23
@@ -101,21 +105,235 @@ __device__ __forceinline__ uint32_t quad_transpose(uint32_t w, uint32_t selA, ui
     return __byte_perm(x, y, selB);
 }
 
+// per-warp epilogue state
+struct EpiWarp {
+    int q, g, lane, u, i4;
+    uint32_t selA, selB;
+    uint8_t *stg;
+    const int32_t *s_key;
+    const uint32_t *s_val;
+    const uint16_t *s_bkt;
+};
+
+// One 32-token chunk of one warp: TMEM columns -> outputs.  m is this
+// lane's weight row, n0 the chunk's first token, c the chunk index within the
+// warp's 64 columns (staging row offset).
+template <int MODE, int OUTK>
+__device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, int32_t adj, float s_in, float cq,
+                                          int64_t n0, int c, const K2Params &P, const EpiParams &E,
+                                          const EpiWarp &W)
+{
+    uint32_t r[32];
+    tc::tmem_ld_32x32b_x32(taddr, r);
+    tc::tmem_ld_wait();
+    int32_t v[32];
+    if constexpr (MODE == EPI_REQUANT) {
+        const int32_t adjM = (int32_t)((uint32_t)adj + (uint32_t)MAGIC_I);
+        const int32_t qoff = MAGIC_I - E.q_zp;
+        float emax = 0.0f;
+        uint32_t umax = 0;
+        const unsigned long long M2 = tc::f2pack(MAGIC_F, MAGIC_F), C2 = tc::f2pack(cq, cq);
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+            const int32_t b0 = (int32_t)(r[j] + (uint32_t)adjM);
+            const int32_t b1 = (int32_t)(r[j + 1] + (uint32_t)adjM);
+            umax = max(umax, (uint32_t)(b0 - 0x4B000000));
+            umax = max(umax, (uint32_t)(b1 - 0x4B000000));
+            const unsigned long long af = tc::sub_f32x2(tc::f2pack(__int_as_float(b0), __int_as_float(b1)), M2);
+            const unsigned long long rf = tc::mul_f32x2(af, C2);
+            const unsigned long long uu = tc::add_f32x2(rf, M2);
+            const unsigned long long d = tc::sub_f32x2(rf, tc::sub_f32x2(uu, M2));
+            emax = fmaxf(emax, __fmaf_rn(fabsf(tc::f2lo(rf)), 9.5367431640625e-07f, fabsf(tc::f2lo(d))));
+            emax = fmaxf(emax, __fmaf_rn(fabsf(tc::f2hi(rf)), 9.5367431640625e-07f, fabsf(tc::f2hi(d))));
+            v[j] = __float_as_int(tc::f2lo(uu)) - qoff;
+            v[j + 1] = __float_as_int(tc::f2hi(uu)) - qoff;
+        }
+        if (__any_sync(0xffffffffu, emax >= 0.5f || umax >= 0x800000u)) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const int32_t a = (int32_t)(r[j] + (uint32_t)adj);
+                const int32_t b = (int32_t)((uint32_t)a + (uint32_t)MAGIC_I);
+                const float rf = __fmul_rn(__fsub_rn(__int_as_float(b), MAGIC_F), cq);
+                const float d = __fsub_rn(rf, __fsub_rn(__fadd_rn(rf, MAGIC_F), MAGIC_F));
+                const bool bad = ((uint32_t)(b - 0x4B000000) >= 0x800000u) ||
+                                 !(__fmaf_rn(fabsf(rf), 9.5367431640625e-07f, fabsf(d)) < 0.5f);
+                if (bad && mok) v[j] = requant_exact(a, s_in, E.q_scale, E.q_zp, E.q_lo, E.q_hi);
+            }
+        }
+        if (OUTK == OUT_32 || OUTK == OUT_8_DIRECT) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = min(max(v[j], E.q_lo), E.q_hi);
+        }
+    } else if constexpr (MODE == EPI_S32) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = (int32_t)(r[j] + (uint32_t)adj);
+    } else if constexpr (MODE == EPI_DEQ_F32) {
+        const int32_t adjM = (int32_t)((uint32_t)adj + (uint32_t)MAGIC_I);
+        uint32_t umax = 0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const int32_t b = (int32_t)(r[j] + (uint32_t)adjM);
+            umax = max(umax, (uint32_t)(b - 0x4B000000));
+            v[j] = __float_as_int(__fmul_rn(__fsub_rn(__int_as_float(b), MAGIC_F), s_in));
+        }
+        if (__any_sync(0xffffffffu, umax >= 0x800000u)) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const int32_t a = (int32_t)(r[j] + (uint32_t)adj);
+                if ((uint32_t)(a + 0x400000) >= 0x800000u) v[j] = __float_as_int(deq_exact(a, s_in));
+            }
+        }
+    } else if constexpr (MODE == EPI_DEQ_TABLE) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const float x = dev_deq_acc((int32_t)(r[j] + (uint32_t)adj), s_in);
+            v[j] = (int32_t)bp_lookup_bucketed(x, W.s_key, W.s_bkt, W.s_val, E.n_bp, E.bp_key_lo, E.bp_shift,
+                                               E.bp_nbucket);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const int64_t n = n0 + j;
+            v[j] = (mok && n < P.N) ? (int32_t)epi_apply<MODE>((int32_t)(r[j] + (uint32_t)adj), m, n, E) : 0;
+        }
+    }
+
+    if constexpr (OUTK == OUT_32) {
+        if (mok) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (n0 + j < P.N) reinterpret_cast<int32_t *>(P.out)[(n0 + j) * P.ldo + m] = v[j];
+        }
+    } else if constexpr (OUTK == OUT_8_DIRECT) {
+        if (mok) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (n0 + j < P.N) reinterpret_cast<uint8_t *>(P.out)[(n0 + j) * P.ldo + m] = (uint8_t)(v[j] & 0xFF);
+        }
+    } else {
+        // saturating pack of 4 consecutive tokens, quad transpose to 4
+        // consecutive m, swizzled STS into the [token][128 m] staging tile
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            uint32_t word;
+            if (OUTK == OUT_U8_TMA)
+                word = tc::pack_sat_u8(v[4 * w + 1], v[4 * w], tc::pack_sat_u8(v[4 * w + 3], v[4 * w + 2], 0));
+            else
+                word = tc::pack_sat_s8(v[4 * w + 1], v[4 * w], tc::pack_sat_s8(v[4 * w + 3], v[4 * w + 2], 0));
+            word = quad_transpose(word, W.selA, W.selB);
+            const int t = c * 32 + 4 * w + W.u;            // token row within the group
+            const int chunk = 2 * W.q + (W.i4 >> 2);         // 16B chunk of the 128B row
+            const int off = t * 128 + ((chunk ^ (t & 7)) << 4) + 4 * (W.i4 & 3);
+            *reinterpret_cast<uint32_t *>(W.stg + off) = word;
+        }
+    }
+}
+
+// Epilogue of one accumulator tile for one warp (its 32 rows x 64 tokens),
+// followed by the release of the accumulator and (8-bit) the TMA store of
+// the group's staging tile.  row0 = first weight row of this CTA's 128-row
+// half, tmem_col = accumulator column base.  release(): arrive on tempty.
+template <int MODE, int OUTK, typename Release>
+__device__ __forceinline__ void epi_tile(uint32_t tmem_base, uint32_t tmem_col, int32_t row0, int64_t tok0,
+                                         const CUtensorMap *tmap_o, const K2Params &P, const EpiParams &E,
+                                         const EpiWarp &W, Release release)
+{
+    constexpr bool STAGED = (OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA);
+    const int32_t m = row0 + W.q * 32 + W.lane;
+    const bool mok = m < E.M;
+    const int32_t adj = mok ? __ldg(E.adj + m) : 0;
+    const float s_in = mok ? __ldg(E.scale_in + m) : 0.0f;
+    float cq = 0.0f;
+    if (MODE == EPI_REQUANT) cq = mok ? __ldg(P.rqc + m) : 0.0f;
+    if (!(P.debug & 1)) {
+#pragma unroll 1
+        for (int c = 0; c < COLS / 32; ++c) {
+            const int col = W.g * COLS + c * 32;
+            epi_chunk<MODE, OUTK>(tmem_base + ((uint32_t)(W.q * 32) << 16) + tmem_col + col, m, mok, adj, s_in, cq,
+                                  tok0 + col, c, P, E, W);
+        }
+    }
+    // this warp's TMEM reads are complete: release the accumulator
+    tc::tc_fence_before();
+    __syncwarp();
+    if (W.lane == 0) release();
+    if constexpr (STAGED) {
+        tc::fence_proxy_async_smem();
+        tc::named_bar_sync(1 + W.g, 128);
+        if (W.q == 2 && W.lane == 0) {
+            tc::tma_store_2d(tmap_o, W.stg, row0, (int32_t)(tok0 + W.g * COLS));
+            tc::tma_store_commit();
+            tc::tma_store_wait_read0();
+        }
+        tc::named_bar_sync(1 + W.g, 128);
+    }
+}
+
+template <int MODE>
+__device__ __forceinline__ EpiWarp make_epi_warp(int warp, int lane, uint8_t *staging, uint8_t *tables,
+                                                 const EpiParams &E)
+{
+    EpiWarp W;
+    W.q = warp & 3;
+    W.g = (warp - 2) >> 2;
+    W.lane = lane;
+    W.u = lane & 3;
+    W.i4 = lane >> 2;
+    W.selA = (W.u & 1) ? 0x3715u : 0x6240u;
+    W.selB = (W.u & 2) ? 0x3276u : 0x5410u;
+    W.stg = staging + W.g * STG_GROUP;
+    int32_t *s_key = reinterpret_cast<int32_t *>(tables);
+    uint32_t *s_val = reinterpret_cast<uint32_t *>(tables + 4 * E.n_bp);
+    uint16_t *s_bkt = reinterpret_cast<uint16_t *>(tables + 8 * E.n_bp + 4);
+    if constexpr (MODE == EPI_DEQ_TABLE) {
+        const int et = threadIdx.x - 64;
+        for (int i = et; i < E.n_bp; i += 32 * EPI_WARPS) s_key[i] = __ldg(E.bp_key + i);
+        for (int i = et; i <= E.n_bp; i += 32 * EPI_WARPS) s_val[i] = __ldg(E.bp_v + i);
+        for (int i = et; i < E.bp_nbucket; i += 32 * EPI_WARPS) s_bkt[i] = __ldg(E.bp_bucket + i);
+        tc::named_bar_sync(1 + EPI_GROUPS, 32 * EPI_WARPS);
+    }
+    W.s_key = s_key;
+    W.s_val = s_val;
+    W.s_bkt = s_bkt;
+    return W;
+}
+
+template <int OUTK>
+constexpr int staged_bytes() { return (OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA) ? STG_BYTES : 0; }
+template <int MODE>
+constexpr int table_bytes() { return MODE == EPI_DEQ_TABLE ? TABLE_BYTES : 0; }
+
+// ================================================================ single CTA
+constexpr int S_BM = 128;
+constexpr int S_A = S_BM * BK;       // 16 KB
+constexpr int S_B = TILE_N * BK;     // 32 KB
+constexpr int S_STAGE = S_A + S_B;
+
+template <int MODE, int OUTK>
+constexpr int single_stages()
+{
+    return (SMEM_MAX - 2048 - staged_bytes<OUTK>() - table_bytes<MODE>()) / S_STAGE > 4
+               ? 4
+               : (SMEM_MAX - 2048 - staged_bytes<OUTK>() - table_bytes<MODE>()) / S_STAGE;
+}
+template <int MODE, int OUTK>
+constexpr int single_smem()
+{
+    return single_stages<MODE, OUTK>() * S_STAGE + staged_bytes<OUTK>() + table_bytes<MODE>() + 1024 + 512;
+}
+
 template <int MODE, int OUTK>
 __global__ void __launch_bounds__(THREADS, 1)
 k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
              const __grid_constant__ CUtensorMap tmap_o, const K2Params P, const EpiParams E)
 {
-    constexpr bool STAGED = (OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA);
-    constexpr int STAGES = stages_for<MODE>();
-    constexpr int SMEM_RING = STAGES * STAGE_BYTES;
+    constexpr int STAGES = single_stages<MODE, OUTK>();
+    constexpr int RING = STAGES * S_STAGE;
     extern __shared__ uint8_t smem_raw[];
-    const uint32_t base_u32 = tc::smem_u32(smem_raw);
-    uint8_t *smem = smem_raw + ((1024 - (base_u32 & 1023)) & 1023);
-    uint8_t *stage_base = smem;
-    uint8_t *staging = smem + SMEM_RING;
-    uint8_t *tables = smem + SMEM_RING + (STAGED ? 2 * STG_HALF : 0);
-    uint64_t *full = reinterpret_cast<uint64_t *>(tables + (MODE == EPI_DEQ_TABLE ? TABLE_BYTES : 0));
+    uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
+    uint8_t *staging = smem + RING;
+    uint8_t *tables = staging + staged_bytes<OUTK>();
+    uint64_t *full = reinterpret_cast<uint64_t *>(tables + table_bytes<MODE>());
     uint64_t *empty = full + STAGES;
     uint64_t *tfull = empty + STAGES;
     uint64_t *tempty = tfull + 2;
@@ -123,7 +341,6 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int total_tiles = P.mtiles * P.ntiles;
-
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             tc::mbar_init(&full[s], 1);
@@ -136,7 +353,6 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
         tc::mbar_fence_init();
         tc::tma_prefetch_desc(&tmap_w);
         tc::tma_prefetch_desc(&tmap_x);
-        if (STAGED) tc::tma_prefetch_desc(&tmap_o);
     }
     if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
     tc::tc_fence_before();
@@ -146,22 +362,26 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
 
     if (warp == 0) {
         if (lane == 0) {
-            // ---------------- TMA producer
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
                 const int mt = tile % P.mtiles, nt = tile / P.mtiles;
                 for (int kc = 0; kc < P.kchunks; ++kc) {
                     tc::mbar_wait(&empty[stage], phase ^ 1);
-                    uint8_t *a_s = stage_base + stage * STAGE_BYTES;
-                    uint8_t *b_s = a_s + A_BYTES;
-                    tc::mbar_expect_tx(&full[stage], STAGE_BYTES);
-                    tc::tma_load_2d(a_s, &tmap_w, &full[stage], mt * BM, kc * BK);
-                    if (P.b_mn_major) {
-                        tc::tma_load_2d(b_s, &tmap_x, &full[stage], nt * BN, kc * BK);
-                        tc::tma_load_2d(b_s + B_BYTES / 2, &tmap_x, &full[stage], nt * BN + 128, kc * BK);
+                    uint8_t *a_s = smem + stage * S_STAGE;
+                    uint8_t *b_s = a_s + S_A;
+                    if (P.debug & 8) {
+                        tc::mbar_arrive(&full[stage]);
                     } else {
-                        tc::tma_load_2d(b_s, &tmap_x, &full[stage], kc * BK, nt * BN);
+                        const int lmt = (P.debug & 2) ? 0 : mt, lnt = (P.debug & 4) ? 0 : nt;
+                        tc::mbar_expect_tx(&full[stage], S_STAGE);
+                        tc::tma_load_2d(a_s, &tmap_w, &full[stage], lmt * S_BM, kc * BK);
+                        if (P.b_mn_major) {
+                            tc::tma_load_2d(b_s, &tmap_x, &full[stage], lnt * TILE_N, kc * BK);
+                            tc::tma_load_2d(b_s + S_B / 2, &tmap_x, &full[stage], lnt * TILE_N + 128, kc * BK);
+                        } else {
+                            tc::tma_load_2d(b_s, &tmap_x, &full[stage], kc * BK, lnt * TILE_N);
+                        }
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -169,27 +389,23 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            // ---------------- MMA issuer (one thread)
-            const uint32_t idesc = tc::idesc_i8(BM, BN, 1, P.b_mn_major ? 1 : 0);
-            int stage = 0;
-            uint32_t phase = 0;
-            int acc = 0;
-            uint32_t acc_phase = 0;
+            const uint32_t idesc = tc::idesc_i8(S_BM, TILE_N, 1, P.b_mn_major ? 1 : 0);
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, acc_phase = 0;
             for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
                 tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * BN;
+                const uint32_t d_tmem = tmem_base + acc * TILE_N;
                 for (int kc = 0; kc < P.kchunks; ++kc) {
                     tc::mbar_wait(&full[stage], phase);
                     tc::tc_fence_after();
-                    const uint32_t a_addr = tc::smem_u32(stage_base + stage * STAGE_BYTES);
-                    const uint32_t b_addr = a_addr + A_BYTES;
+                    const uint32_t a_addr = tc::smem_u32(smem + stage * S_STAGE);
+                    const uint32_t b_addr = a_addr + S_A;
 #pragma unroll
-                    for (int kk = 0; kk < BK / 32; ++kk) {
-                        const uint64_t adesc = tc::smem_desc_sw128(a_addr + kk * 4096, A_BYTES, 1024);
-                        const uint64_t bdesc = P.b_mn_major
-                                                   ? tc::smem_desc_sw128(b_addr + kk * 4096, B_BYTES / 2, 1024)
-                                                   : tc::smem_desc_sw128(b_addr + kk * 32, 16, 1024);
+                    for (int kk = 0; kk < ((P.debug & 16) ? 0 : BK / 32); ++kk) {
+                        const uint64_t adesc = tc::smem_desc_sw128(a_addr + kk * 4096, S_A, 1024);
+                        const uint64_t bdesc = P.b_mn_major ? tc::smem_desc_sw128(b_addr + kk * 4096, S_B / 2, 1024)
+                                                            : tc::smem_desc_sw128(b_addr + kk * 32, 16, 1024);
                         tc::mma_i8(d_tmem, adesc, bdesc, idesc, (kc | kk) ? 1u : 0u);
                     }
                     tc::mma_commit(&empty[stage]);
@@ -201,168 +417,220 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
             }
         }
     } else {
-        // ---------------- epilogue warps
-        const int q = warp & 3;             // TMEM lane quarter this warp may access (m sub-block)
-        const int h = (warp - 2) >> 2;      // token half of the 256-token tile
-        const int u = lane & 3, i4 = lane >> 2;
-        const uint32_t selA = (u & 1) ? 0x3715u : 0x6240u;
-        const uint32_t selB = (u & 2) ? 0x3276u : 0x5410u;
-        uint8_t *stg = staging + h * STG_HALF;
-        // breakpoint tables -> smem (keys | values | buckets)
-        int32_t *s_key = reinterpret_cast<int32_t *>(tables);
-        uint32_t *s_val = reinterpret_cast<uint32_t *>(tables + 4 * E.n_bp);
-        uint16_t *s_bkt = reinterpret_cast<uint16_t *>(tables + 8 * E.n_bp + 4);
-        if constexpr (MODE == EPI_DEQ_TABLE) {
-            const int et = threadIdx.x - 64;
-            for (int i = et; i < E.n_bp; i += 32 * EPI_WARPS) s_key[i] = __ldg(E.bp_key + i);
-            for (int i = et; i <= E.n_bp; i += 32 * EPI_WARPS) s_val[i] = __ldg(E.bp_v + i);
-            for (int i = et; i < E.bp_nbucket; i += 32 * EPI_WARPS) s_bkt[i] = __ldg(E.bp_bucket + i);
-            tc::named_bar_sync(3, 32 * EPI_WARPS);
-        }
-        const bool leader = (q == ((2 + 4 * h) & 3)) && lane == 0;  // first warp of the half
+        const EpiWarp W = make_epi_warp<MODE>(warp, lane, staging, tables, E);
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
             const int mt = tile % P.mtiles, nt = tile / P.mtiles;
-            const int32_t m = mt * BM + q * 32 + lane;
-            const bool mok = m < E.M;
-            const int32_t adj = mok ? __ldg(E.adj + m) : 0;
-            const float s_in = mok ? __ldg(E.scale_in + m) : 0.0f;
-            float cq = 0.0f;
-            if (MODE == EPI_REQUANT) cq = mok ? __ldg(P.rqc + m) : 0.0f;
             tc::mbar_wait(&tfull[acc], acc_phase);
             tc::tc_fence_after();
-#pragma unroll 1
-            for (int c = 0; c < 128 / 32; ++c) {
-                const int col = h * 128 + c * 32;
-                uint32_t r[32];
-                tc::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + col, r);
-                tc::tmem_ld_wait();
-                const int64_t n0 = (int64_t)nt * BN + col;
-                int32_t v[32];
-                if constexpr (MODE == EPI_REQUANT) {
-                    const int32_t adjM = (int32_t)((uint32_t)adj + (uint32_t)MAGIC_I);
-                    const int32_t qoff = MAGIC_I - E.q_zp;
-                    float emax = 0.0f;
-                    uint32_t umax = 0;
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int32_t b = (int32_t)(r[j] + (uint32_t)adjM);
-                        umax = max(umax, (uint32_t)(b - 0x4B000000));
-                        const float af = __fsub_rn(__int_as_float(b), MAGIC_F);
-                        const float rf = __fmul_rn(af, cq);
-                        const float uu = __fadd_rn(rf, MAGIC_F);
-                        const float d = __fsub_rn(rf, __fsub_rn(uu, MAGIC_F));
-                        emax = fmaxf(emax, __fmaf_rn(fabsf(rf), 9.5367431640625e-07f, fabsf(d)));
-                        v[j] = __float_as_int(uu) - qoff;
-                    }
-                    if (__any_sync(0xffffffffu, emax >= 0.5f || umax >= 0x800000u)) {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const int32_t a = (int32_t)(r[j] + (uint32_t)adj);
-                            const int32_t b = (int32_t)((uint32_t)a + (uint32_t)MAGIC_I);
-                            const float rf = __fmul_rn(__fsub_rn(__int_as_float(b), MAGIC_F), cq);
-                            const float d = __fsub_rn(rf, __fsub_rn(__fadd_rn(rf, MAGIC_F), MAGIC_F));
-                            const bool bad = ((uint32_t)(b - 0x4B000000) >= 0x800000u) ||
-                                             !(__fmaf_rn(fabsf(rf), 9.5367431640625e-07f, fabsf(d)) < 0.5f);
-                            if (bad && mok) v[j] = requant_exact(a, s_in, E.q_scale, E.q_zp, E.q_lo, E.q_hi);
-                        }
-                    }
-                    if (OUTK == OUT_32 || OUTK == OUT_8_DIRECT) {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) v[j] = min(max(v[j], E.q_lo), E.q_hi);
-                    }
-                } else if constexpr (MODE == EPI_S32) {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = (int32_t)(r[j] + (uint32_t)adj);
-                } else if constexpr (MODE == EPI_DEQ_F32) {
-                    const int32_t adjM = (int32_t)((uint32_t)adj + (uint32_t)MAGIC_I);
-                    uint32_t umax = 0;
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int32_t b = (int32_t)(r[j] + (uint32_t)adjM);
-                        umax = max(umax, (uint32_t)(b - 0x4B000000));
-                        v[j] = __float_as_int(__fmul_rn(__fsub_rn(__int_as_float(b), MAGIC_F), s_in));
-                    }
-                    if (__any_sync(0xffffffffu, umax >= 0x800000u)) {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const int32_t a = (int32_t)(r[j] + (uint32_t)adj);
-                            if ((uint32_t)(a + 0x400000) >= 0x800000u) v[j] = __float_as_int(deq_exact(a, s_in));
-                        }
-                    }
-                } else if constexpr (MODE == EPI_DEQ_TABLE) {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const float x = dev_deq_acc((int32_t)(r[j] + (uint32_t)adj), s_in);
-                        v[j] = (int32_t)bp_lookup_bucketed(x, s_key, s_bkt, s_val, E.n_bp, E.bp_key_lo, E.bp_shift,
-                                                           E.bp_nbucket);
-                    }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int64_t n = n0 + j;
-                        v[j] = (mok && n < P.N)
-                                   ? (int32_t)epi_apply<MODE>((int32_t)(r[j] + (uint32_t)adj), m, n, E)
-                                   : 0;
-                    }
-                }
-
-                if constexpr (OUTK == OUT_32) {
-                    if (mok) {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (n0 + j < P.N) reinterpret_cast<int32_t *>(P.out)[(n0 + j) * P.ldo + m] = v[j];
-                    }
-                } else if constexpr (OUTK == OUT_8_DIRECT) {
-                    if (mok) {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (n0 + j < P.N)
-                                reinterpret_cast<uint8_t *>(P.out)[(n0 + j) * P.ldo + m] = (uint8_t)(v[j] & 0xFF);
-                    }
-                } else {
-                    // saturating pack of 4 consecutive tokens, quad transpose to
-                    // 4 consecutive m, swizzled STS into the [token][128 m] tile
-#pragma unroll
-                    for (int w = 0; w < 8; ++w) {
-                        uint32_t word;
-                        if (OUTK == OUT_U8_TMA)
-                            word = tc::pack_sat_u8(v[4 * w + 1], v[4 * w], tc::pack_sat_u8(v[4 * w + 3], v[4 * w + 2], 0));
-                        else
-                            word = tc::pack_sat_s8(v[4 * w + 1], v[4 * w], tc::pack_sat_s8(v[4 * w + 3], v[4 * w + 2], 0));
-                        word = quad_transpose(word, selA, selB);
-                        const int t = c * 32 + 4 * w + u;                // token row within the half
-                        const int chunk = 2 * q + (i4 >> 2);              // 16B chunk of the 128B row
-                        const int off = t * 128 + (((chunk ^ (t & 7)) << 4)) + 4 * (i4 & 3);
-                        *reinterpret_cast<uint32_t *>(stg + off) = word;
-                    }
-                }
-            }
-            // this warp's TMEM reads are complete: release the accumulator
-            tc::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&tempty[acc]);
-            if constexpr (STAGED) {
-                tc::fence_proxy_async_smem();
-                tc::named_bar_sync(1 + h, 128);
-                if (leader) {
-                    tc::tma_store_2d(&tmap_o, stg, mt * BM, nt * BN + h * 128);
-                    tc::tma_store_commit();
-                    tc::tma_store_wait_read0();
-                }
-                tc::named_bar_sync(1 + h, 128);
-            }
+            uint64_t *te = &tempty[acc];
+            epi_tile<MODE, OUTK>(tmem_base, acc * TILE_N, mt * S_BM, (int64_t)nt * TILE_N, &tmap_o, P, E, W,
+                                 [te] { tc::mbar_arrive(te); });
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
-        if (STAGED && leader) tc::tma_store_wait_all0();
+        if ((OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA) && W.q == 2 && lane == 0) tc::tma_store_wait_all0();
     }
     tc::tc_fence_before();
     __syncthreads();
     if (warp == 1) {
         tc::tc_fence_after();
         tc::tmem_dealloc(tmem_base, 512);
+    }
+}
+
+// ================================================================ CTA pair
+// Per CTA: A half = 128 W rows x 128 k (16 KB), B half = 128 tokens x 128 k
+// (16 KB).  X-stationary: B halves for all k chunks stay resident.
+constexpr int P_A = 128 * BK;        // 16 KB
+constexpr int P_B = 128 * BK;        // 16 KB
+constexpr int KMAX_XSTAT = 1024;     // resident X: 128 tokens x K <= 128 KB per CTA
+
+template <int MODE, int OUTK, bool XSTAT>
+constexpr int pair_stages()
+{
+    constexpr int fixed = staged_bytes<OUTK>() + table_bytes<MODE>() + 2048 + (XSTAT ? KMAX_XSTAT * 128 : 0);
+    constexpr int per = XSTAT ? P_A : (P_A + P_B);
+    constexpr int s = (SMEM_MAX - fixed) / per;
+    return s > 8 ? 8 : s;
+}
+template <int MODE, int OUTK, bool XSTAT>
+constexpr int pair_smem()
+{
+    return pair_stages<MODE, OUTK, XSTAT>() * (XSTAT ? P_A : P_A + P_B) + (XSTAT ? KMAX_XSTAT * 128 : 0) +
+           staged_bytes<OUTK>() + table_bytes<MODE>() + 1024 + 512;
+}
+
+template <int MODE, int OUTK, bool XSTAT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
+           const __grid_constant__ CUtensorMap tmap_o, const K2Params P, const EpiParams E)
+{
+    constexpr int STAGES = pair_stages<MODE, OUTK, XSTAT>();
+    constexpr int SLOT = XSTAT ? P_A : (P_A + P_B);
+    constexpr int XBYTES = XSTAT ? KMAX_XSTAT * 128 : 0;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
+    uint8_t *xbuf = smem;                            // XSTAT: [kchunks][128 tok x 128 k]
+    uint8_t *ring = smem + XBYTES;
+    uint8_t *staging = ring + STAGES * SLOT;
+    uint8_t *tables = staging + staged_bytes<OUTK>();
+    uint64_t *full = reinterpret_cast<uint64_t *>(tables + table_bytes<MODE>());
+    uint64_t *empty = full + STAGES;
+    uint64_t *tfull = empty + STAGES;
+    uint64_t *tempty = tfull + 2;
+    uint64_t *xfull = tempty + 2;
+    uint64_t *xempty = xfull + 1;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(xempty + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = tc::cluster_ctarank();
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    // work units: XSTAT -> (token tile, m-group); else (token tile, m-tile), m fastest
+    const int units = XSTAT ? P.ntiles * P.mgroups : P.ntiles * P.mtiles;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            tc::mbar_init(&tfull[a], 1);
+            tc::mbar_init(&tempty[a], 2 * EPI_WARPS);
+        }
+        tc::mbar_init(xfull, 1);
+        tc::mbar_init(xempty, 1);
+        tc::mbar_fence_init();
+        tc::tma_prefetch_desc(&tmap_w);
+        tc::tma_prefetch_desc(&tmap_x);
+    }
+    if (warp == 1) tc::tmem_alloc_2sm(tmem_slot, 512);
+    tc::tc_fence_before();
+    tc::cluster_sync();
+    tc::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    auto unit_range = [&](int unit, int &nt, int &m_lo, int &m_hi) {
+        if (XSTAT) {
+            nt = unit / P.mgroups;
+            const int mg = unit % P.mgroups;
+            const int base = P.mtiles / P.mgroups, rem = P.mtiles % P.mgroups;
+            m_lo = mg * base + (mg < rem ? mg : rem);
+            m_hi = m_lo + base + (mg < rem ? 1 : 0);
+        } else {
+            nt = unit / P.mtiles;
+            m_lo = unit % P.mtiles;
+            m_hi = m_lo + 1;
+        }
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer (both CTAs; bytes land on the leader's barriers)
+            const uint32_t full0 = tc::mapa(tc::smem_u32(full), 0);
+            const uint32_t xfull0 = tc::mapa(tc::smem_u32(xfull), 0);
+            int stage = 0;
+            uint32_t phase = 0, xphase = 0;
+            for (int unit = pair; unit < units; unit += npairs) {
+                int nt, m_lo, m_hi;
+                unit_range(unit, nt, m_lo, m_hi);
+                const int tok = nt * TILE_N + 128 * (int)rank;
+                if (XSTAT) {
+                    tc::mbar_wait_cluster(xempty, xphase ^ 1);
+                    if (rank == 0) tc::mbar_expect_tx(xfull, 2 * P.kchunks * P_B);
+                    for (int kc = 0; kc < P.kchunks; ++kc) {
+                        if (P.b_mn_major)
+                            tc::tma_load_2d_2sm(xbuf + kc * P_B, &tmap_x, xfull0, tok, kc * BK);
+                        else
+                            tc::tma_load_2d_2sm(xbuf + kc * P_B, &tmap_x, xfull0, kc * BK, tok);
+                    }
+                    xphase ^= 1;
+                }
+                for (int mt = m_lo; mt < m_hi; ++mt) {
+                    for (int kc = 0; kc < P.kchunks; ++kc) {
+                        tc::mbar_wait_cluster(&empty[stage], phase ^ 1);
+                        uint8_t *a_s = ring + stage * SLOT;
+                        const uint32_t fb = full0 + 8 * stage;
+                        if (rank == 0) tc::mbar_expect_tx(&full[stage], 2 * SLOT);
+                        tc::tma_load_2d_2sm(a_s, &tmap_w, fb, mt * 256 + 128 * (int)rank, kc * BK);
+                        if (!XSTAT) {
+                            if (P.b_mn_major)
+                                tc::tma_load_2d_2sm(a_s + P_A, &tmap_x, fb, tok, kc * BK);
+                            else
+                                tc::tma_load_2d_2sm(a_s + P_A, &tmap_x, fb, kc * BK, tok);
+                        }
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            // ---------------- MMA issuer: leader CTA, one thread, M256 x N256 x K32
+            const uint32_t idesc = tc::idesc_i8(256, TILE_N, 1, P.b_mn_major ? 1 : 0);
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, acc_phase = 0, xphase = 0;
+            for (int unit = pair; unit < units; unit += npairs) {
+                int nt, m_lo, m_hi;
+                unit_range(unit, nt, m_lo, m_hi);
+                if (XSTAT) {
+                    tc::mbar_wait(xfull, xphase);
+                    xphase ^= 1;
+                    tc::tc_fence_after();
+                }
+                for (int mt = m_lo; mt < m_hi; ++mt) {
+                    tc::mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+                    tc::tc_fence_after();
+                    const uint32_t d_tmem = tmem_base + acc * TILE_N;
+                    for (int kc = 0; kc < P.kchunks; ++kc) {
+                        tc::mbar_wait(&full[stage], phase);
+                        tc::tc_fence_after();
+                        const uint32_t a_addr = tc::smem_u32(ring + stage * SLOT);
+                        const uint32_t b_addr = XSTAT ? tc::smem_u32(xbuf + kc * P_B) : a_addr + P_A;
+#pragma unroll
+                        for (int kk = 0; kk < ((P.debug & 16) ? 0 : BK / 32); ++kk) {
+                            const uint64_t adesc = tc::smem_desc_sw128(a_addr + kk * 4096, P_A, 1024);
+                            const uint64_t bdesc = P.b_mn_major ? tc::smem_desc_sw128(b_addr + kk * 4096, P_B, 1024)
+                                                                : tc::smem_desc_sw128(b_addr + kk * 32, 16, 1024);
+                            tc::mma_i8_2sm(d_tmem, adesc, bdesc, idesc, (kc | kk) ? 1u : 0u);
+                        }
+                        tc::mma_commit_2sm_mc(&empty[stage], 0x3);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                    tc::mma_commit_2sm_mc(&tfull[acc], 0x3);
+                    acc ^= 1;
+                    if (acc == 0) acc_phase ^= 1;
+                }
+                if (XSTAT) tc::mma_commit_2sm_mc(xempty, 0x3);
+            }
+        }
+    } else {
+        // ---------------- epilogue warps (both CTAs; each reads its own TMEM half)
+        const EpiWarp W = make_epi_warp<MODE>(warp, lane, staging, tables, E);
+        const uint32_t tempty0 = tc::mapa(tc::smem_u32(tempty), 0);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int unit = pair; unit < units; unit += npairs) {
+            int nt, m_lo, m_hi;
+            unit_range(unit, nt, m_lo, m_hi);
+            for (int mt = m_lo; mt < m_hi; ++mt) {
+                tc::mbar_wait_cluster(&tfull[acc], acc_phase);
+                tc::tc_fence_after();
+                const uint32_t te = tempty0 + 8 * acc;
+                epi_tile<MODE, OUTK>(tmem_base, acc * TILE_N, mt * 256 + 128 * (int)rank, (int64_t)nt * TILE_N,
+                                     &tmap_o, P, E, W, [te] { tc::mbar_arrive_cluster(te); });
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+        if ((OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA) && W.q == 2 && lane == 0) tc::tma_store_wait_all0();
+    }
+    tc::tc_fence_before();
+    tc::cluster_sync();
+    if (warp == 1) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc_2sm(tmem_base, 512);
     }
 }
 
@@ -410,42 +678,80 @@ bool encode_2d(CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t outer, 
     cuuint64_t strides[1] = {pitch_bytes};
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(ptr), dims, strides,
-                                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(ptr), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
-template <int MODE, int OUTK>
-int launch_mode(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx, const CUtensorMap &to,
-                const K2Params &p)
+int env_int(const char *name, int dflt)
 {
-    auto kern = k2_tc_kernel<MODE, OUTK>;
-    constexpr int smem = smem_bytes<MODE, OUTK>();
-    static_assert(smem <= 232448, "shared memory budget");
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr_set = true;
-    }
+    const char *e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
+enum Variant { V_SINGLE = 0, V_PAIR = 1, V_PAIR_XSTAT = 2 };
+
+template <int MODE, int OUTK>
+int launch_mode(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx, const CUtensorMap &to, K2Params p,
+                int variant)
+{
     EpiParams E = make_epi(a.h, a.img, a.sides, a.n);
-    const int tiles = p.mtiles * p.ntiles;
-    const int grid = tiles < num_sms() ? tiles : num_sms();
-    kern<<<grid, THREADS, smem, (cudaStream_t)a.stream>>>(tw, tx, to, p, E);
+    cudaStream_t st = (cudaStream_t)a.stream;
+    const int sms = num_sms();
+    if (variant == V_SINGLE) {
+        auto kern = k2_tc_kernel<MODE, OUTK>;
+        constexpr int smem = single_smem<MODE, OUTK>();
+        static_assert(smem <= SMEM_MAX, "shared memory budget");
+        static bool attr = false;
+        if (!attr) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); attr = true; }
+        const int tiles = p.mtiles * p.ntiles;
+        kern<<<tiles < sms ? tiles : sms, THREADS, smem, st>>>(tw, tx, to, p, E);
+    } else if (variant == V_PAIR) {
+        auto kern = k2p_kernel<MODE, OUTK, false>;
+        constexpr int smem = pair_smem<MODE, OUTK, false>();
+        static_assert(smem <= SMEM_MAX, "shared memory budget");
+        static bool attr = false;
+        if (!attr) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); attr = true; }
+        const int units = p.mtiles * p.ntiles;
+        const int pairs = units < sms / 2 ? units : sms / 2;
+        kern<<<2 * pairs, THREADS, smem, st>>>(tw, tx, to, p, E);
+    } else {
+        auto kern = k2p_kernel<MODE, OUTK, true>;
+        constexpr int smem = pair_smem<MODE, OUTK, true>();
+        static_assert(smem <= SMEM_MAX, "shared memory budget");
+        static bool attr = false;
+        if (!attr) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); attr = true; }
+        // split each token tile's m-tiles into groups so units load-balance
+        // over the pairs: minimise waves * (m-tiles per unit + X reload cost)
+        const int npairs = sms / 2;
+        int best_g = 1;
+        double best = 1e30;
+        for (int g = 1; g <= p.mtiles; ++g) {
+            const long units = (long)p.ntiles * g;
+            const long waves = (units + npairs - 1) / npairs;
+            const double cost = (double)waves * ((double)((p.mtiles + g - 1) / g) + 0.25);
+            if (cost < best - 1e-9) { best = cost; best_g = g; }
+        }
+        p.mgroups = best_g;
+        const long units = (long)p.ntiles * best_g;
+        const int pairs = units < npairs ? (int)units : npairs;
+        kern<<<2 * pairs, THREADS, smem, st>>>(tw, tx, to, p, E);
+    }
     return (int)cudaGetLastError();
 }
 
 template <int OUTK>
 int launch_outk(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx, const CUtensorMap &to,
-                const K2Params &p)
+                const K2Params &p, int variant)
 {
     switch (a.h->epi_mode) {
-    case EPI_S32: return launch_mode<EPI_S32, OUTK>(a, tw, tx, to, p);
-    case EPI_DEQ_F32: return launch_mode<EPI_DEQ_F32, OUTK>(a, tw, tx, to, p);
-    case EPI_REQUANT: return launch_mode<EPI_REQUANT, OUTK>(a, tw, tx, to, p);
-    case EPI_REQUANT_LUT: return launch_mode<EPI_REQUANT_LUT, OUTK>(a, tw, tx, to, p);
-    case EPI_DEQ_TABLE: return launch_mode<EPI_DEQ_TABLE, OUTK>(a, tw, tx, to, p);
-    default: return launch_mode<EPI_GENERIC, OUTK>(a, tw, tx, to, p);
+    case EPI_S32: return launch_mode<EPI_S32, OUTK>(a, tw, tx, to, p, variant);
+    case EPI_DEQ_F32: return launch_mode<EPI_DEQ_F32, OUTK>(a, tw, tx, to, p, variant);
+    case EPI_REQUANT: return launch_mode<EPI_REQUANT, OUTK>(a, tw, tx, to, p, variant);
+    case EPI_REQUANT_LUT: return launch_mode<EPI_REQUANT_LUT, OUTK>(a, tw, tx, to, p, variant);
+    case EPI_DEQ_TABLE: return launch_mode<EPI_DEQ_TABLE, OUTK>(a, tw, tx, to, p, variant);
+    default: return launch_mode<EPI_GENERIC, OUTK>(a, tw, tx, to, p, variant);
     }
 }
 
@@ -453,7 +759,7 @@ int launch_outk(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx,
 
 bool k2_supported(const SiImage *h, int64_t n, int32_t layout, const void *x, int64_t ldx, int64_t)
 {
-    if (n < 1 || n > (int64_t)INT32_MAX - BN) return false;
+    if (n < 1 || n > (int64_t)INT32_MAX - TILE_N) return false;
     if (((uintptr_t)x) % 16) return false;
     if (ldx % 16) return false;
     if (layout == 1 && h->K % 16) return false;  // K-major rows: TMA inner extent granularity
@@ -467,35 +773,51 @@ int k2_launch_count(const SiImage *, int32_t) { return 1; }
 int k2_launch(const SpmmArgs &a)
 {
     const SiImage *h = a.h;
+    static const int dbg = env_int("SI_K2_DEBUG", 0);
+    static const int forced = [] {
+        const char *e = getenv("SI_K2_VARIANT");
+        if (!e) return -1;
+        std::string s(e);
+        return s == "single" ? (int)V_SINGLE : s == "pair" ? (int)V_PAIR : s == "xstat" ? (int)V_PAIR_XSTAT : -1;
+    }();
+    // the pair kernels tile W rows by 256; an odd count of 128-row tiles reads
+    // one tile of TMA out-of-bounds zero fill
+    int variant = forced >= 0 ? forced : (h->tc_kpad <= KMAX_XSTAT ? V_PAIR_XSTAT : V_PAIR);
+    if (variant == V_PAIR_XSTAT && h->tc_kpad > KMAX_XSTAT) variant = V_PAIR;
+
     CUtensorMap tw, tx, to;
     const void *wt = img_sec<uint8_t>(a.img, h->off_tc_wt);
     const uint64_t mpad = (uint64_t)h->tc_mtiles * 128;
     if (!encode_2d(&tw, wt, mpad, (uint64_t)h->tc_kpad, mpad, 128, BK)) return (int)cudaErrorInvalidValue;
+    const uint32_t xbox_tok = variant == V_SINGLE ? TILE_N : 128;
     bool ok;
     if (a.layout == 0)
         ok = encode_2d(&tx, a.x, (uint64_t)a.n, (uint64_t)h->K, (uint64_t)a.ldx, 128, BK);
     else
-        ok = encode_2d(&tx, a.x, (uint64_t)h->K, (uint64_t)a.n, (uint64_t)a.ldx, BK, BN);
+        ok = encode_2d(&tx, a.x, (uint64_t)h->K, (uint64_t)a.n, (uint64_t)a.ldx, BK, xbox_tok);
     if (!ok) return (int)cudaErrorInvalidValue;
     K2Params p;
-    p.mtiles = h->tc_mtiles;
-    p.ntiles = (int32_t)((a.n + BN - 1) / BN);
+    p.mtiles = variant == V_SINGLE ? h->tc_mtiles : (h->tc_mtiles + 1) / 2;
+    p.ntiles = (int32_t)((a.n + TILE_N - 1) / TILE_N);
     p.kchunks = h->tc_kpad / BK;
     p.b_mn_major = a.layout == 0 ? 1 : 0;
+    p.mgroups = 1;
     p.N = a.n;
     p.out = a.out;
     p.ldo = a.ldo;
     p.rqc = img_sec<float>(a.img, h->off_rqc);
+    p.debug = dbg;
     const bool out32 = h->out_dtype == 0 || h->out_dtype == 3;
     if (out32) {
         std::memset(&to, 0, sizeof(to));
-        return launch_outk<OUT_32>(a, tw, tx, to, p);
+        return launch_outk<OUT_32>(a, tw, tx, to, p, variant);
     }
     const bool tma_ok = (a.ldo % 16 == 0) && ((uintptr_t)a.out % 16 == 0) &&
-                        encode_2d(&to, a.out, (uint64_t)h->M, (uint64_t)a.n, (uint64_t)a.ldo, 128, 128);
+                        encode_2d(&to, a.out, (uint64_t)h->M, (uint64_t)a.n, (uint64_t)a.ldo, 128, COLS);
     if (!tma_ok) {
         std::memset(&to, 0, sizeof(to));
-        return launch_outk<OUT_8_DIRECT>(a, tw, tx, to, p);
+        return launch_outk<OUT_8_DIRECT>(a, tw, tx, to, p, variant);
     }
-    return h->out_dtype == 2 ? launch_outk<OUT_U8_TMA>(a, tw, tx, to, p) : launch_outk<OUT_S8_TMA>(a, tw, tx, to, p);
+    return h->out_dtype == 2 ? launch_outk<OUT_U8_TMA>(a, tw, tx, to, p, variant)
+                             : launch_outk<OUT_S8_TMA>(a, tw, tx, to, p, variant);
 }
