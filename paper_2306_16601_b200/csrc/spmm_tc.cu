@@ -233,18 +233,26 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, i
 // followed by the release of the accumulator and (8-bit) the TMA store of
 // the group's staging tile.  row0 = first weight row of this CTA's 128-row
 // half, tmem_col = accumulator column base.  release(): arrive on tempty.
-template <int MODE, int OUTK, typename Release>
+template <int MODE, int OUTK, typename Wait, typename Release>
 __device__ __forceinline__ void epi_tile(uint32_t tmem_base, uint32_t tmem_col, int32_t row0, int64_t tok0,
                                          const CUtensorMap *tmap_o, const K2Params &P, const EpiParams &E,
-                                         const EpiWarp &W, Release release)
+                                         const EpiWarp &W, Wait wait_full, Release release)
 {
     constexpr bool STAGED = (OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA);
     const int32_t m = row0 + W.q * 32 + W.lane;
     const bool mok = m < E.M;
+    // per-row constants: issue the loads before blocking on the accumulator
     const int32_t adj = mok ? __ldg(E.adj + m) : 0;
     const float s_in = mok ? __ldg(E.scale_in + m) : 0.0f;
     float cq = 0.0f;
     if (MODE == EPI_REQUANT) cq = mok ? __ldg(P.rqc + m) : 0.0f;
+    wait_full();
+    tc::tc_fence_after();
+    if constexpr (STAGED) {
+        // the previous tile's TMA store must have finished reading the staging tile
+        if (W.q == 2 && W.lane == 0) tc::tma_store_wait_read0();
+        tc::named_bar_sync(1 + W.g, 128);
+    }
     if (!(P.debug & 1)) {
 #pragma unroll 1
         for (int c = 0; c < COLS / 32; ++c) {
@@ -263,9 +271,7 @@ __device__ __forceinline__ void epi_tile(uint32_t tmem_base, uint32_t tmem_col, 
         if (W.q == 2 && W.lane == 0) {
             tc::tma_store_2d(tmap_o, W.stg, row0, (int32_t)(tok0 + W.g * COLS));
             tc::tma_store_commit();
-            tc::tma_store_wait_read0();
         }
-        tc::named_bar_sync(1 + W.g, 128);
     }
 }
 
@@ -367,7 +373,7 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
             for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
                 const int mt = tile % P.mtiles, nt = tile / P.mtiles;
                 for (int kc = 0; kc < P.kchunks; ++kc) {
-                    tc::mbar_wait(&empty[stage], phase ^ 1);
+                    tc::mbar_spin(&empty[stage], phase ^ 1);
                     uint8_t *a_s = smem + stage * S_STAGE;
                     uint8_t *b_s = a_s + S_A;
                     if (P.debug & 8) {
@@ -393,11 +399,11 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
             for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-                tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc::mbar_spin(&tempty[acc], acc_phase ^ 1);
                 tc::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * TILE_N;
                 for (int kc = 0; kc < P.kchunks; ++kc) {
-                    tc::mbar_wait(&full[stage], phase);
+                    tc::mbar_spin(&full[stage], phase);
                     tc::tc_fence_after();
                     const uint32_t a_addr = tc::smem_u32(smem + stage * S_STAGE);
                     const uint32_t b_addr = a_addr + S_A;
@@ -422,11 +428,11 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
         uint32_t acc_phase = 0;
         for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
             const int mt = tile % P.mtiles, nt = tile / P.mtiles;
-            tc::mbar_wait(&tfull[acc], acc_phase);
-            tc::tc_fence_after();
             uint64_t *te = &tempty[acc];
+            uint64_t *tf = &tfull[acc];
+            const uint32_t ph = acc_phase;
             epi_tile<MODE, OUTK>(tmem_base, acc * TILE_N, mt * S_BM, (int64_t)nt * TILE_N, &tmap_o, P, E, W,
-                                 [te] { tc::mbar_arrive(te); });
+                                 [tf, ph] { tc::mbar_wait(tf, ph); }, [te] { tc::mbar_arrive(te); });
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
@@ -470,6 +476,7 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
     constexpr int STAGES = pair_stages<MODE, OUTK, XSTAT>();
     constexpr int SLOT = XSTAT ? P_A : (P_A + P_B);
     constexpr int XBYTES = XSTAT ? KMAX_XSTAT * 128 : 0;
+    constexpr int XCH = KMAX_XSTAT / BK;             // 8 resident X chunks
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t *xbuf = smem;                            // XSTAT: [kchunks][128 tok x 128 k]
@@ -480,9 +487,9 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
     uint64_t *empty = full + STAGES;
     uint64_t *tfull = empty + STAGES;
     uint64_t *tempty = tfull + 2;
-    uint64_t *xfull = tempty + 2;
-    uint64_t *xempty = xfull + 1;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(xempty + 1);
+    uint64_t *xfull = tempty + 2;                    // per K chunk of the resident X tile
+    uint64_t *xempty = xfull + XCH;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(xempty + XCH);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = tc::cluster_ctarank();
@@ -499,8 +506,10 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
             tc::mbar_init(&tfull[a], 1);
             tc::mbar_init(&tempty[a], 2 * EPI_WARPS);
         }
-        tc::mbar_init(xfull, 1);
-        tc::mbar_init(xempty, 1);
+        for (int c = 0; c < XCH; ++c) {
+            tc::mbar_init(&xfull[c], 1);
+            tc::mbar_init(&xempty[c], 1);
+        }
         tc::mbar_fence_init();
         tc::tma_prefetch_desc(&tmap_w);
         tc::tma_prefetch_desc(&tmap_x);
@@ -536,20 +545,19 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
                 int nt, m_lo, m_hi;
                 unit_range(unit, nt, m_lo, m_hi);
                 const int tok = nt * TILE_N + 128 * (int)rank;
-                if (XSTAT) {
-                    tc::mbar_wait_cluster(xempty, xphase ^ 1);
-                    if (rank == 0) tc::mbar_expect_tx(xfull, 2 * P.kchunks * P_B);
-                    for (int kc = 0; kc < P.kchunks; ++kc) {
-                        if (P.b_mn_major)
-                            tc::tma_load_2d_2sm(xbuf + kc * P_B, &tmap_x, xfull0, tok, kc * BK);
-                        else
-                            tc::tma_load_2d_2sm(xbuf + kc * P_B, &tmap_x, xfull0, kc * BK, tok);
-                    }
-                    xphase ^= 1;
-                }
                 for (int mt = m_lo; mt < m_hi; ++mt) {
                     for (int kc = 0; kc < P.kchunks; ++kc) {
-                        tc::mbar_wait_cluster(&empty[stage], phase ^ 1);
+                        if (XSTAT && mt == m_lo) {
+                            // roll the resident X tile chunk by chunk: chunk kc is
+                            // reloaded as soon as the previous unit's last MMA on it retires
+                            tc::mbar_spin(&xempty[kc], xphase ^ 1);
+                            if (rank == 0) tc::mbar_expect_tx(&xfull[kc], 2 * P_B);
+                            if (P.b_mn_major)
+                                tc::tma_load_2d_2sm(xbuf + kc * P_B, &tmap_x, xfull0 + 8 * kc, tok, kc * BK);
+                            else
+                                tc::tma_load_2d_2sm(xbuf + kc * P_B, &tmap_x, xfull0 + 8 * kc, kc * BK, tok);
+                        }
+                        tc::mbar_spin(&empty[stage], phase ^ 1);
                         uint8_t *a_s = ring + stage * SLOT;
                         const uint32_t fb = full0 + 8 * stage;
                         if (rank == 0) tc::mbar_expect_tx(&full[stage], 2 * SLOT);
@@ -563,6 +571,7 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                 }
+                xphase ^= 1;
             }
         }
     } else if (warp == 1) {
@@ -574,17 +583,13 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
             for (int unit = pair; unit < units; unit += npairs) {
                 int nt, m_lo, m_hi;
                 unit_range(unit, nt, m_lo, m_hi);
-                if (XSTAT) {
-                    tc::mbar_wait(xfull, xphase);
-                    xphase ^= 1;
-                    tc::tc_fence_after();
-                }
                 for (int mt = m_lo; mt < m_hi; ++mt) {
-                    tc::mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+                    tc::mbar_spin(&tempty[acc], acc_phase ^ 1);
                     tc::tc_fence_after();
                     const uint32_t d_tmem = tmem_base + acc * TILE_N;
                     for (int kc = 0; kc < P.kchunks; ++kc) {
-                        tc::mbar_wait(&full[stage], phase);
+                        if (XSTAT && mt == m_lo) tc::mbar_spin(&xfull[kc], xphase);
+                        tc::mbar_spin(&full[stage], phase);
                         tc::tc_fence_after();
                         const uint32_t a_addr = tc::smem_u32(ring + stage * SLOT);
                         const uint32_t b_addr = XSTAT ? tc::smem_u32(xbuf + kc * P_B) : a_addr + P_A;
@@ -596,13 +601,14 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
                             tc::mma_i8_2sm(d_tmem, adesc, bdesc, idesc, (kc | kk) ? 1u : 0u);
                         }
                         tc::mma_commit_2sm_mc(&empty[stage], 0x3);
+                        if (XSTAT && mt == m_hi - 1) tc::mma_commit_2sm_mc(&xempty[kc], 0x3);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                     tc::mma_commit_2sm_mc(&tfull[acc], 0x3);
                     acc ^= 1;
                     if (acc == 0) acc_phase ^= 1;
                 }
-                if (XSTAT) tc::mma_commit_2sm_mc(xempty, 0x3);
+                xphase ^= 1;
             }
         }
     } else {
@@ -615,11 +621,12 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
             int nt, m_lo, m_hi;
             unit_range(unit, nt, m_lo, m_hi);
             for (int mt = m_lo; mt < m_hi; ++mt) {
-                tc::mbar_wait_cluster(&tfull[acc], acc_phase);
-                tc::tc_fence_after();
                 const uint32_t te = tempty0 + 8 * acc;
+                uint64_t *tf = &tfull[acc];
+                const uint32_t ph = acc_phase;
                 epi_tile<MODE, OUTK>(tmem_base, acc * TILE_N, mt * 256 + 128 * (int)rank, (int64_t)nt * TILE_N,
-                                     &tmap_o, P, E, W, [te] { tc::mbar_arrive_cluster(te); });
+                                     &tmap_o, P, E, W, [tf, ph] { tc::mbar_wait(tf, ph); },
+                                     [te] { tc::mbar_arrive_cluster(te); });
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }

@@ -253,3 +253,30 @@ __device__ __forceinline__ void mma_commit_2sm_mc(uint64_t *bar, uint16_t cta_ma
         : "memory");
 }
 }  // namespace tc
+
+namespace tc {
+// non-sleeping waits for the single-thread producer / MMA roles: test_wait
+// polls without the suspend of try_wait, so a phase flip is seen within a
+// few cycles (the roles are one thread each, the issue slots they use are
+// negligible next to the 16 epilogue warps)
+__device__ __forceinline__ void mbar_spin(uint64_t *b, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "SPIN_%=:\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra SPIN_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_spin_cluster(uint64_t *b, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "SPINC_%=:\n\t"
+        "mbarrier.test_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra SPINC_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+}  // namespace tc
