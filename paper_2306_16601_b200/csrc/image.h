@@ -63,6 +63,16 @@ struct SiImage {
     int32_t bp_key_lo, bp_shift, bp_nbucket, pad2;
     uint64_t off_bp_key;     // i32   [n_bp]            threshold keys
     uint64_t off_bp_bucket;  // u16   [bp_nbucket]      first threshold index per key bucket
+    // K2 on-chip expansion lists: for every (128-row tile rt, 128-k chunk kc,
+    // 64-k half) the nonzero 4x1 blocks as smem word offsets into the
+    // MN-major SWIZZLE_128B [128 k x 128 m] operand tile plus the 4-row value
+    // word.  List j: u32 values[n] then u16 offsets[n], n padded to 8 by
+    // repeating the last entry, starting at byte tc_eptr[j].
+    int32_t tc_emax;         // max padded entries of any list
+    int32_t tc_nlists;       // tc_mtiles * kchunks * 2
+    uint64_t off_tc_eptr;    // u32   [tc_nlists + 1]   byte offsets into the entry section
+    uint64_t off_tc_ent;     // bytes                   entry lists
+    uint64_t reserved2;
 };
 
 static_assert(sizeof(SiImage) % 16 == 0, "image header must stay 16-byte aligned");

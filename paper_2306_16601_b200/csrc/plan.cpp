@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <algorithm>
 #include <cfloat>
 #include <string>
 #include <vector>
@@ -264,9 +265,81 @@ Compiled compile_program(const si_program *p)
 }
 
 struct Layout {
-    uint64_t off[18];
+    uint64_t off[20];
     uint64_t total;
 };
+
+// K2 expansion lists (see image.h).  Blocks are bucketed by (row tile, k
+// chunk, k half); duplicate (group, column) pairs are summed per row with
+// int8 wrap-around, as decode_sparse's np.add.at does (sparse.py:130-131).
+struct ExpandLists {
+    std::vector<uint32_t> ptr;   // byte offsets, size nlists + 1
+    std::vector<uint8_t> bytes;
+    int32_t emax = 0;
+};
+
+ExpandLists build_expand_lists(const si_weight *w)
+{
+    ExpandLists e;
+    const int32_t G = w->rows / 4;
+    const int32_t rt_n = (w->logical_rows + 127) / 128;
+    const int32_t kch = (w->cols + 127) / 128;
+    const int64_t nlists = (int64_t)rt_n * kch * 2;
+    std::vector<std::vector<std::pair<uint16_t, uint32_t>>> lists((size_t)nlists);
+    for (int32_t g = 0; g < G; ++g) {
+        const int32_t rt = g / 32, gl = g % 32;
+        if (rt >= rt_n) break;
+        // accumulate this group's blocks by column (handles duplicates)
+        std::vector<std::pair<int32_t, uint32_t>> cols;
+        for (int64_t q = w->group_ptr[g]; q < w->group_ptr[g + 1]; ++q) {
+            uint8_t b[4];
+            bool any = false;
+            for (int r = 0; r < 4; ++r) {
+                b[r] = (uint8_t)w->vals[(q / 4) * 16 + r * 4 + (q % 4)];
+                if (g * 4 + r >= w->logical_rows) b[r] = 0;
+                any |= b[r] != 0;
+            }
+            if (!any) continue;
+            const uint32_t word = (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) | ((uint32_t)b[3] << 24);
+            bool merged = false;
+            for (auto &c : cols)
+                if (c.first == w->idx[q]) {
+                    uint32_t o = c.second, sum = 0;
+                    for (int r = 0; r < 4; ++r)
+                        sum |= (uint32_t)(uint8_t)((int8_t)(o >> (8 * r)) + (int8_t)(word >> (8 * r))) << (8 * r);
+                    c.second = sum;
+                    merged = true;
+                    break;
+                }
+            if (!merged) cols.emplace_back(w->idx[q], word);
+        }
+        for (auto &c : cols) {
+            const int32_t k = c.first, kc = k / 128, kl = k % 128, half = kl / 64;
+            const int32_t ml = 4 * gl;
+            const uint32_t byte = (uint32_t)kl * 128 + ((((uint32_t)ml >> 4) ^ ((uint32_t)kl & 7)) << 4) + (ml & 15);
+            lists[((size_t)rt * kch + kc) * 2 + half].emplace_back((uint16_t)(byte / 4), c.second);
+        }
+    }
+    e.ptr.assign((size_t)nlists + 1, 0);
+    for (int64_t j = 0; j < nlists; ++j) {
+        auto &L = lists[(size_t)j];
+        std::sort(L.begin(), L.end());
+        const size_t n = L.size(), n8 = (n + 7) / 8 * 8;
+        e.ptr[(size_t)j] = (uint32_t)e.bytes.size();
+        e.emax = std::max<int32_t>(e.emax, (int32_t)n8);
+        for (size_t i = 0; i < n8; ++i) {
+            const uint32_t v = L[std::min(i, n - 1)].second;
+            for (int bb = 0; bb < 4; ++bb) e.bytes.push_back((uint8_t)(v >> (8 * bb)));
+        }
+        for (size_t i = 0; i < n8; ++i) {
+            const uint16_t o = L[std::min(i, n - 1)].first;
+            e.bytes.push_back((uint8_t)o);
+            e.bytes.push_back((uint8_t)(o >> 8));
+        }
+    }
+    e.ptr[(size_t)nlists] = (uint32_t)e.bytes.size();
+    return e;
+}
 
 }  // namespace
 
@@ -322,7 +395,7 @@ static int32_t validate(const si_weight *w, const si_program *p)
     return SI_OK;
 }
 
-static Layout make_layout(const si_weight *w, const si_program *p, const Compiled &c)
+static Layout make_layout(const si_weight *w, const si_program *p, const Compiled &c, const ExpandLists &x)
 {
     Layout l{};
     const int64_t G = w->rows / 4, T = w->group_ptr[G], tiles = T / 4;
@@ -348,6 +421,8 @@ static Layout make_layout(const si_weight *w, const si_program *p, const Compile
     put(15, 4 * M);
     put(16, 4 * c.bp.x.size());
     put(17, 2 * c.bp_bucket.size());
+    put(18, 4 * x.ptr.size());
+    put(19, x.bytes.size());
     l.total = cur;
     return l;
 }
@@ -357,7 +432,8 @@ extern "C" int32_t si_plan_image_size(const si_weight *w, const si_program *p, u
     int32_t rc = validate(w, p);
     if (rc) return rc;
     Compiled c = compile_program(p);
-    *bytes = make_layout(w, p, c).total;
+    ExpandLists x = build_expand_lists(w);
+    *bytes = make_layout(w, p, c, x).total;
     return SI_OK;
 }
 
@@ -367,7 +443,8 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
     int32_t rc = validate(w, p);
     if (rc) return rc;
     Compiled c = compile_program(p);
-    Layout l = make_layout(w, p, c);
+    ExpandLists x = build_expand_lists(w);
+    Layout l = make_layout(w, p, c, x);
     if (bytes < l.total) { si_set_error("image buffer too small"); return SI_ENOSPACE; }
     uint8_t *base = (uint8_t *)host_image;
     std::memset(base, 0, l.total);
@@ -394,6 +471,12 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
     h->bp_key_lo = c.bp_key_lo;
     h->bp_shift = c.bp_shift;
     h->bp_nbucket = (int32_t)c.bp_bucket.size();
+    h->off_tc_eptr = l.off[18];
+    h->off_tc_ent = l.off[19];
+    h->tc_emax = x.emax;
+    h->tc_nlists = (int32_t)(x.ptr.size() - 1);
+    std::memcpy(base + h->off_tc_eptr, x.ptr.data(), 4 * x.ptr.size());
+    if (!x.bytes.empty()) std::memcpy(base + h->off_tc_ent, x.bytes.data(), x.bytes.size());
 
     // micro-tiles: reference layout kept verbatim (sparse.py:28-31)
     int32_t *tp = (int32_t *)(base + h->off_tile_ptr);

@@ -78,6 +78,7 @@ struct K2Params {
     void *out;
     int64_t ldo;
     const float *rqc;    // requant c[m] = f32(scale_in[m] / fp)
+    int32_t rtiles;      // 128-row weight tiles with expansion lists (k2x)
     int32_t debug;       // experiment switches (SI_K2_DEBUG): 1 skip epilogue, 2 W tile 0 only,
                          // 4 X tile 0 only, 8 no TMA, 16 no MMA
 };
@@ -641,6 +642,259 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
     }
 }
 
+
+// ================================================================ CTA pair, expanded W
+// As k2p, but the weight operand never streams densely: per (128-row tile,
+// 128-k chunk) the plan holds the nonzero 4x1 blocks as (smem word offset,
+// 4-row value word) lists (csrc/plan.cpp build_expand_lists).  The producer
+// bulk-copies a stage's two lists (k rows 0-63 / 64-127) into an entry ring;
+// two expander warps zero their half of the MN-major SWIZZLE_128B A tile and
+// scatter the words.  W traffic per token tile drops from M*K bytes to
+// ~6 bytes per nonzero block, and a stage is ready a few hundred cycles after
+// its lists land instead of after a 16 KB L2->smem TMA round trip.
+struct XLayout {
+    int32_t nstages;      // W (and streamed-X) ring slots
+    int32_t neslots;      // entry-list ring slots
+    int32_t eslot_bytes;  // bytes per entry slot (two half lists)
+    int32_t ehalf_bytes;  // offset of the second half list in a slot
+    int32_t xbytes;       // resident X bytes (X-stationary) or 0
+    int32_t slot_bytes;   // W (+X) bytes per ring slot
+    int32_t staged;       // staging bytes
+    int32_t tables;       // table bytes
+};
+constexpr int X_MAXSLOTS = 8;
+constexpr int EXP_WARPS = 2;
+constexpr int X_THREADS = THREADS + 32 * EXP_WARPS;
+
+template <int MODE, int OUTK, bool XSTAT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(X_THREADS, 1)
+k2x_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_o, const K2Params P,
+           const EpiParams E, const XLayout L, const uint32_t *__restrict__ eptr, const uint8_t *__restrict__ ent)
+{
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
+    uint8_t *xbuf = smem;
+    uint8_t *ring = smem + L.xbytes;
+    uint8_t *staging = ring + L.nstages * L.slot_bytes;
+    uint8_t *tables = staging + L.staged;
+    uint8_t *eslots = tables + L.tables;
+    uint64_t *full = reinterpret_cast<uint64_t *>(eslots + L.neslots * L.eslot_bytes);
+    uint64_t *empty = full + X_MAXSLOTS;
+    uint64_t *efull = empty + X_MAXSLOTS;
+    uint64_t *eempty = efull + X_MAXSLOTS;
+    uint64_t *tfull = eempty + X_MAXSLOTS;
+    uint64_t *tempty = tfull + 2;
+    uint64_t *xfull = tempty + 2;
+    uint64_t *xempty = xfull + 8;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(xempty + 8);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = tc::cluster_ctarank();
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int units = XSTAT ? P.ntiles * P.mgroups : P.ntiles * P.mtiles;
+    const int S = L.nstages, ES = L.neslots;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            tc::mbar_init(&full[s], 2 * EXP_WARPS + (XSTAT ? 0 : 1));
+            tc::mbar_init(&empty[s], 1);
+        }
+        for (int e = 0; e < ES; ++e) {
+            tc::mbar_init(&efull[e], 1);
+            tc::mbar_init(&eempty[e], EXP_WARPS);
+        }
+        for (int a = 0; a < 2; ++a) {
+            tc::mbar_init(&tfull[a], 1);
+            tc::mbar_init(&tempty[a], 2 * EPI_WARPS);
+        }
+        for (int c = 0; c < 8; ++c) {
+            tc::mbar_init(&xfull[c], 1);
+            tc::mbar_init(&xempty[c], 1);
+        }
+        tc::mbar_fence_init();
+        tc::tma_prefetch_desc(&tmap_x);
+    }
+    if (warp == 1) tc::tmem_alloc_2sm(tmem_slot, 512);
+    tc::tc_fence_before();
+    tc::cluster_sync();
+    tc::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    auto unit_range = [&](int unit, int &nt, int &m_lo, int &m_hi) {
+        if (XSTAT) {
+            nt = unit / P.mgroups;
+            const int mg = unit % P.mgroups;
+            const int base = P.mtiles / P.mgroups, rem = P.mtiles % P.mgroups;
+            m_lo = mg * base + (mg < rem ? mg : rem);
+            m_hi = m_lo + base + (mg < rem ? 1 : 0);
+        } else {
+            nt = unit / P.mtiles;
+            m_lo = unit % P.mtiles;
+            m_hi = m_lo + 1;
+        }
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- producer: entry lists (own CTA) + X (TMA, bytes on the leader)
+            const uint32_t full0 = tc::mapa(tc::smem_u32(full), 0);
+            const uint32_t xfull0 = tc::mapa(tc::smem_u32(xfull), 0);
+            int stage = 0, es = 0;
+            uint32_t phase = 0, ephase = 0, xphase = 0;
+            for (int unit = pair; unit < units; unit += npairs) {
+                int nt, m_lo, m_hi;
+                unit_range(unit, nt, m_lo, m_hi);
+                const int tok = nt * TILE_N + 128 * (int)rank;
+                for (int mt = m_lo; mt < m_hi; ++mt) {
+                    const int rt = 2 * mt + (int)rank;
+                    for (int kc = 0; kc < P.kchunks; ++kc) {
+                        // entry lists of this CTA's half of the stage
+                        tc::mbar_spin(&eempty[es], ephase ^ 1);
+                        uint32_t b0 = 0, b1 = 0, o0 = 0, o1 = 0;
+                        if (rt < P.rtiles) {
+                            const int j = (rt * P.kchunks + kc) * 2;
+                            o0 = __ldg(eptr + j);
+                            o1 = __ldg(eptr + j + 1);
+                            b0 = o1 - o0;
+                            b1 = __ldg(eptr + j + 2) - o1;
+                        }
+                        tc::mbar_expect_tx(&efull[es], b0 + b1);
+                        uint8_t *dst = eslots + es * L.eslot_bytes;
+                        if (b0) tc::bulk_load(dst, ent + o0, b0, &efull[es]);
+                        if (b1) tc::bulk_load(dst + L.ehalf_bytes, ent + o1, b1, &efull[es]);
+                        if (++es == ES) { es = 0; ephase ^= 1; }
+                        if (XSTAT) {
+                            if (mt == m_lo) {
+                                tc::mbar_spin(&xempty[kc], xphase ^ 1);
+                                if (rank == 0) tc::mbar_expect_tx(&xfull[kc], 2 * P_B);
+                                if (P.b_mn_major)
+                                    tc::tma_load_2d_2sm(xbuf + kc * P_B, &tmap_x, xfull0 + 8 * kc, tok, kc * BK);
+                                else
+                                    tc::tma_load_2d_2sm(xbuf + kc * P_B, &tmap_x, xfull0 + 8 * kc, kc * BK, tok);
+                            }
+                        } else {
+                            tc::mbar_spin(&empty[stage], phase ^ 1);
+                            uint8_t *b_s = ring + stage * L.slot_bytes + P_A;
+                            const uint32_t fb = full0 + 8 * stage;
+                            if (rank == 0) tc::mbar_expect_tx(&full[stage], 2 * P_B);
+                            if (P.b_mn_major)
+                                tc::tma_load_2d_2sm(b_s, &tmap_x, fb, tok, kc * BK);
+                            else
+                                tc::tma_load_2d_2sm(b_s, &tmap_x, fb, kc * BK, tok);
+                            if (++stage == S) { stage = 0; phase ^= 1; }
+                        }
+                    }
+                }
+                xphase ^= 1;
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            // ---------------- MMA issuer: leader CTA, one thread, M256 x N256 x K32
+            const uint32_t idesc = tc::idesc_i8(256, TILE_N, 1, P.b_mn_major ? 1 : 0);
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, acc_phase = 0, xphase = 0;
+            for (int unit = pair; unit < units; unit += npairs) {
+                int nt, m_lo, m_hi;
+                unit_range(unit, nt, m_lo, m_hi);
+                for (int mt = m_lo; mt < m_hi; ++mt) {
+                    tc::mbar_spin(&tempty[acc], acc_phase ^ 1);
+                    tc::tc_fence_after();
+                    const uint32_t d_tmem = tmem_base + acc * TILE_N;
+                    for (int kc = 0; kc < P.kchunks; ++kc) {
+                        if (XSTAT && mt == m_lo) tc::mbar_spin(&xfull[kc], xphase);
+                        tc::mbar_spin(&full[stage], phase);
+                        tc::tc_fence_after();
+                        const uint32_t a_addr = tc::smem_u32(ring + stage * L.slot_bytes);
+                        const uint32_t b_addr = XSTAT ? tc::smem_u32(xbuf + kc * P_B) : a_addr + P_A;
+#pragma unroll
+                        for (int kk = 0; kk < ((P.debug & 16) ? 0 : BK / 32); ++kk) {
+                            const uint64_t adesc = tc::smem_desc_sw128(a_addr + kk * 4096, P_A, 1024);
+                            const uint64_t bdesc = P.b_mn_major ? tc::smem_desc_sw128(b_addr + kk * 4096, P_B, 1024)
+                                                                : tc::smem_desc_sw128(b_addr + kk * 32, 16, 1024);
+                            tc::mma_i8_2sm(d_tmem, adesc, bdesc, idesc, (kc | kk) ? 1u : 0u);
+                        }
+                        tc::mma_commit_2sm_mc(&empty[stage], 0x3);
+                        if (XSTAT && mt == m_hi - 1) tc::mma_commit_2sm_mc(&xempty[kc], 0x3);
+                        if (++stage == S) { stage = 0; phase ^= 1; }
+                    }
+                    tc::mma_commit_2sm_mc(&tfull[acc], 0x3);
+                    acc ^= 1;
+                    if (acc == 0) acc_phase ^= 1;
+                }
+                xphase ^= 1;
+            }
+        }
+    } else if (warp >= 2 + EPI_WARPS) {
+        // ---------------- expanders: warp h owns k rows [64h, 64h + 64) of each A tile
+        const int h = warp - (2 + EPI_WARPS);
+        const uint32_t full0 = tc::mapa(tc::smem_u32(full), 0);
+        int stage = 0, es = 0;
+        uint32_t phase = 0, ephase = 0;
+        for (int unit = pair; unit < units; unit += npairs) {
+            int nt, m_lo, m_hi;
+            unit_range(unit, nt, m_lo, m_hi);
+            for (int mt = m_lo; mt < m_hi; ++mt) {
+                const int rt = 2 * mt + (int)rank;
+                for (int kc = 0; kc < P.kchunks; ++kc) {
+                    int n = 0;
+                    if (rt < P.rtiles) {
+                        const int j = (rt * P.kchunks + kc) * 2 + h;
+                        n = (int)((__ldg(eptr + j + 1) - __ldg(eptr + j)) / 6);
+                    }
+                    tc::mbar_wait(&efull[es], ephase);
+                    tc::mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t *a_s = ring + stage * L.slot_bytes;
+                    uint4 *z = reinterpret_cast<uint4 *>(a_s + h * (P_A / 2));
+#pragma unroll 4
+                    for (int i = lane; i < P_A / 2 / 16; i += 32) z[i] = make_uint4(0, 0, 0, 0);
+                    __syncwarp();
+                    const uint8_t *el = eslots + es * L.eslot_bytes + h * L.ehalf_bytes;
+                    const uint32_t *vals = reinterpret_cast<const uint32_t *>(el);
+                    const uint16_t *offs = reinterpret_cast<const uint16_t *>(el + 4 * n);
+                    uint32_t *w32 = reinterpret_cast<uint32_t *>(a_s);
+                    for (int i = lane; i < n; i += 32) w32[offs[i]] = vals[i];
+                    tc::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tc::mbar_arrive(&eempty[es]);
+                        tc::mbar_arrive_cluster(full0 + 8 * stage);
+                    }
+                    if (++es == ES) { es = 0; ephase ^= 1; }
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else {
+        // ---------------- epilogue warps (both CTAs; each reads its own TMEM half)
+        const EpiWarp W = make_epi_warp<MODE>(warp, lane, staging, tables, E);
+        const uint32_t tempty0 = tc::mapa(tc::smem_u32(tempty), 0);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int unit = pair; unit < units; unit += npairs) {
+            int nt, m_lo, m_hi;
+            unit_range(unit, nt, m_lo, m_hi);
+            for (int mt = m_lo; mt < m_hi; ++mt) {
+                const uint32_t te = tempty0 + 8 * acc;
+                uint64_t *tf = &tfull[acc];
+                const uint32_t ph = acc_phase;
+                epi_tile<MODE, OUTK>(tmem_base, acc * TILE_N, mt * 256 + 128 * (int)rank, (int64_t)nt * TILE_N,
+                                     &tmap_o, P, E, W, [tf, ph] { tc::mbar_wait(tf, ph); },
+                                     [te] { tc::mbar_arrive_cluster(te); });
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+        if ((OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA) && W.q == 2 && lane == 0) tc::tma_store_wait_all0();
+    }
+    tc::tc_fence_before();
+    tc::cluster_sync();
+    if (warp == 1) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc_2sm(tmem_base, 512);
+    }
+}
+
 // ---- host side ------------------------------------------------------------------
 int g_num_sms = 0;
 std::once_flag g_sms_once;
@@ -697,7 +951,48 @@ int env_int(const char *name, int dflt)
     return e ? atoi(e) : dflt;
 }
 
-enum Variant { V_SINGLE = 0, V_PAIR = 1, V_PAIR_XSTAT = 2 };
+enum Variant { V_SINGLE = 0, V_PAIR = 1, V_PAIR_XSTAT = 2, V_EXPAND = 3, V_EXPAND_XSTAT = 4 };
+
+int pick_mgroups(int mtiles, int ntiles, int npairs)
+{
+    // split each token tile's m-tiles into groups so units load-balance over
+    // the pairs: minimise waves * (m-tiles per unit + X reload cost)
+    int best_g = 1;
+    double best = 1e30;
+    for (int g = 1; g <= mtiles; ++g) {
+        const long units = (long)ntiles * g;
+        const long waves = (units + npairs - 1) / npairs;
+        const double cost = (double)waves * ((double)((mtiles + g - 1) / g) + 0.25);
+        if (cost < best - 1e-9) { best = cost; best_g = g; }
+    }
+    return best_g;
+}
+
+// shared-memory plan of k2x for this image; false if it does not fit
+template <int MODE, int OUTK>
+bool plan_xlayout(const SiImage *h, bool xstat, XLayout &L, int &smem)
+{
+    const int kch = h->tc_kpad / BK;
+    L.staged = staged_bytes<OUTK>();
+    L.tables = table_bytes<MODE>();
+    L.xbytes = xstat ? kch * P_B : 0;
+    L.slot_bytes = xstat ? P_A : P_A + P_B;
+    L.ehalf_bytes = ((h->tc_emax * 6 + 127) / 128) * 128;
+    L.eslot_bytes = 2 * L.ehalf_bytes;
+    const int fixed = 1024 + 1024 + L.xbytes + L.staged + L.tables;
+    for (int es = 4; es >= 2; --es) {
+        const int room = SMEM_MAX - fixed - es * L.eslot_bytes;
+        int st = room / L.slot_bytes;
+        if (st > 6) st = 6;
+        if (st >= 2) {
+            L.nstages = st;
+            L.neslots = es;
+            smem = fixed + es * L.eslot_bytes + st * L.slot_bytes;
+            return true;
+        }
+    }
+    return false;
+}
 
 template <int MODE, int OUTK>
 int launch_mode(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx, const CUtensorMap &to, K2Params p,
@@ -706,6 +1001,30 @@ int launch_mode(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx,
     EpiParams E = make_epi(a.h, a.img, a.sides, a.n);
     cudaStream_t st = (cudaStream_t)a.stream;
     const int sms = num_sms();
+    if (variant == V_EXPAND || variant == V_EXPAND_XSTAT) {
+        const bool xstat = variant == V_EXPAND_XSTAT;
+        XLayout L;
+        int smem = 0;
+        if (!plan_xlayout<MODE, OUTK>(a.h, xstat, L, smem)) variant = xstat ? V_PAIR_XSTAT : V_PAIR;
+        else {
+            const uint32_t *eptr = img_sec<uint32_t>(a.img, a.h->off_tc_eptr);
+            const uint8_t *ent = img_sec<uint8_t>(a.img, a.h->off_tc_ent);
+            const int npairs = sms / 2;
+            if (xstat) p.mgroups = pick_mgroups(p.mtiles, p.ntiles, npairs);
+            const long units = xstat ? (long)p.ntiles * p.mgroups : (long)p.ntiles * p.mtiles;
+            const int pairs = units < npairs ? (int)units : npairs;
+            if (xstat) {
+                auto kern = k2x_kernel<MODE, OUTK, true>;
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                kern<<<2 * pairs, X_THREADS, smem, st>>>(tx, to, p, E, L, eptr, ent);
+            } else {
+                auto kern = k2x_kernel<MODE, OUTK, false>;
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                kern<<<2 * pairs, X_THREADS, smem, st>>>(tx, to, p, E, L, eptr, ent);
+            }
+            return (int)cudaGetLastError();
+        }
+    }
     if (variant == V_SINGLE) {
         auto kern = k2_tc_kernel<MODE, OUTK>;
         constexpr int smem = single_smem<MODE, OUTK>();
@@ -729,19 +1048,9 @@ int launch_mode(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx,
         static_assert(smem <= SMEM_MAX, "shared memory budget");
         static bool attr = false;
         if (!attr) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); attr = true; }
-        // split each token tile's m-tiles into groups so units load-balance
-        // over the pairs: minimise waves * (m-tiles per unit + X reload cost)
         const int npairs = sms / 2;
-        int best_g = 1;
-        double best = 1e30;
-        for (int g = 1; g <= p.mtiles; ++g) {
-            const long units = (long)p.ntiles * g;
-            const long waves = (units + npairs - 1) / npairs;
-            const double cost = (double)waves * ((double)((p.mtiles + g - 1) / g) + 0.25);
-            if (cost < best - 1e-9) { best = cost; best_g = g; }
-        }
-        p.mgroups = best_g;
-        const long units = (long)p.ntiles * best_g;
+        p.mgroups = pick_mgroups(p.mtiles, p.ntiles, npairs);
+        const long units = (long)p.ntiles * p.mgroups;
         const int pairs = units < npairs ? (int)units : npairs;
         kern<<<2 * pairs, THREADS, smem, st>>>(tw, tx, to, p, E);
     }
@@ -785,12 +1094,14 @@ int k2_launch(const SpmmArgs &a)
         const char *e = getenv("SI_K2_VARIANT");
         if (!e) return -1;
         std::string s(e);
-        return s == "single" ? (int)V_SINGLE : s == "pair" ? (int)V_PAIR : s == "xstat" ? (int)V_PAIR_XSTAT : -1;
+        return s == "single" ? (int)V_SINGLE : s == "pair" ? (int)V_PAIR : s == "xstat" ? (int)V_PAIR_XSTAT
+             : s == "expand" ? (int)V_EXPAND : s == "expand_xstat" ? (int)V_EXPAND_XSTAT : -1;
     }();
     // the pair kernels tile W rows by 256; an odd count of 128-row tiles reads
     // one tile of TMA out-of-bounds zero fill
-    int variant = forced >= 0 ? forced : (h->tc_kpad <= KMAX_XSTAT ? V_PAIR_XSTAT : V_PAIR);
+    int variant = forced >= 0 ? forced : (h->tc_kpad <= KMAX_XSTAT ? V_EXPAND_XSTAT : V_EXPAND);
     if (variant == V_PAIR_XSTAT && h->tc_kpad > KMAX_XSTAT) variant = V_PAIR;
+    if (variant == V_EXPAND_XSTAT && h->tc_kpad > KMAX_XSTAT) variant = V_EXPAND;
 
     CUtensorMap tw, tx, to;
     const void *wt = img_sec<uint8_t>(a.img, h->off_tc_wt);
@@ -813,6 +1124,7 @@ int k2_launch(const SpmmArgs &a)
     p.out = a.out;
     p.ldo = a.ldo;
     p.rqc = img_sec<float>(a.img, h->off_rqc);
+    p.rtiles = h->tc_mtiles;
     p.debug = dbg;
     const bool out32 = h->out_dtype == 0 || h->out_dtype == 3;
     if (out32) {

@@ -280,3 +280,14 @@ __device__ __forceinline__ void mbar_spin_cluster(uint64_t *b, uint32_t parity)
         : "memory");
 }
 }  // namespace tc
+
+namespace tc {
+// 1-D bulk copy global -> this CTA's smem, completing bytes on an mbarrier
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"((uint64_t)src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+}  // namespace tc
