@@ -66,7 +66,7 @@ constexpr int STG_BYTES = EPI_GROUPS * STG_GROUP;
 constexpr int TABLE_BYTES = 16 * 1024;      // breakpoint tables staged in smem (EPI_DEQ_TABLE)
 constexpr int SMEM_MAX = 232448;
 
-enum OutKind { OUT_32 = 0, OUT_U8_TMA = 1, OUT_S8_TMA = 2, OUT_8_DIRECT = 3 };
+enum OutKind { OUT_32 = 0, OUT_U8_TMA = 1, OUT_S8_TMA = 2, OUT_8_DIRECT = 3, OUT_U8_Q = 4, OUT_S8_Q = 5 };
 
 struct K2Params {
     int32_t mtiles;      // weight-row tiles (128 rows single-CTA, 256 rows per pair)
@@ -210,6 +210,32 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, i
 #pragma unroll
             for (int j = 0; j < 32; ++j)
                 if (n0 + j < P.N) reinterpret_cast<uint8_t *>(P.out)[(n0 + j) * P.ldo + m] = (uint8_t)(v[j] & 0xFF);
+        }
+    } else if constexpr (OUTK == OUT_U8_Q || OUTK == OUT_S8_Q) {
+        // saturating pack of 4 consecutive tokens, quad transpose to 4
+        // consecutive m, one 32-bit store per 4 outputs: each warp store
+        // covers 4 token rows x 32 contiguous bytes (full sectors)
+        const int32_t mq = m - W.lane + 4 * W.i4;
+        uint8_t *o8 = reinterpret_cast<uint8_t *>(P.out);
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            uint32_t word;
+            if (OUTK == OUT_U8_Q)
+                word = tc::pack_sat_u8(v[4 * w + 1], v[4 * w], tc::pack_sat_u8(v[4 * w + 3], v[4 * w + 2], 0));
+            else
+                word = tc::pack_sat_s8(v[4 * w + 1], v[4 * w], tc::pack_sat_s8(v[4 * w + 3], v[4 * w + 2], 0));
+            word = quad_transpose(word, W.selA, W.selB);
+            const int64_t n = n0 + 4 * w + W.u;
+            if (n < P.N) {
+                uint8_t *dst = o8 + n * P.ldo + mq;
+                if (mq + 3 < E.M) {
+                    *reinterpret_cast<uint32_t *>(dst) = word;
+                } else {
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+                        if (mq + b < E.M) dst[b] = (uint8_t)(word >> (8 * b));
+                }
+            }
         }
     } else {
         // saturating pack of 4 consecutive tokens, quad transpose to 4
@@ -662,7 +688,7 @@ struct XLayout {
     int32_t staged;       // staging bytes
     int32_t tables;       // table bytes
 };
-constexpr int X_MAXSLOTS = 8;
+constexpr int X_MAXSLOTS = 12;
 constexpr int EXP_WARPS = 2;
 constexpr int X_THREADS = THREADS + 32 * EXP_WARPS;
 
@@ -696,12 +722,12 @@ k2x_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ C
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
-            tc::mbar_init(&full[s], 2 * EXP_WARPS + (XSTAT ? 0 : 1));
+            tc::mbar_init(&full[s], 2 + (XSTAT ? 0 : 1));
             tc::mbar_init(&empty[s], 1);
         }
         for (int e = 0; e < ES; ++e) {
             tc::mbar_init(&efull[e], 1);
-            tc::mbar_init(&eempty[e], EXP_WARPS);
+            tc::mbar_init(&eempty[e], 1);
         }
         for (int a = 0; a < 2; ++a) {
             tc::mbar_init(&tfull[a], 1);
@@ -826,42 +852,62 @@ k2x_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ C
             }
         }
     } else if (warp >= 2 + EPI_WARPS) {
-        // ---------------- expanders: warp h owns k rows [64h, 64h + 64) of each A tile
-        const int h = warp - (2 + EPI_WARPS);
+        // ---------------- expanders: warp e builds every EXP_WARPS-th stage's
+        // whole A tile (zero 16 KB, scatter the two half lists), so each warp
+        // has EXP_WARPS MMA-stage times to finish one stage
+        const int e = warp - (2 + EPI_WARPS);
         const uint32_t full0 = tc::mapa(tc::smem_u32(full), 0);
-        int stage = 0, es = 0;
-        uint32_t phase = 0, ephase = 0;
+        long it = 0;  // global stage counter (same sequence as producer / MMA)
         for (int unit = pair; unit < units; unit += npairs) {
             int nt, m_lo, m_hi;
             unit_range(unit, nt, m_lo, m_hi);
             for (int mt = m_lo; mt < m_hi; ++mt) {
                 const int rt = 2 * mt + (int)rank;
-                for (int kc = 0; kc < P.kchunks; ++kc) {
-                    int n = 0;
+                for (int kc = 0; kc < P.kchunks; ++kc, ++it) {
+                    if ((int)(it % EXP_WARPS) != e) continue;
+                    const int stage = (int)(it % S), es = (int)(it % ES);
+                    const uint32_t phase = (uint32_t)((it / S) & 1), ephase = (uint32_t)((it / ES) & 1);
+                    int n0 = 0, n1 = 0;
                     if (rt < P.rtiles) {
-                        const int j = (rt * P.kchunks + kc) * 2 + h;
-                        n = (int)((__ldg(eptr + j + 1) - __ldg(eptr + j)) / 6);
+                        const int j = (rt * P.kchunks + kc) * 2;
+                        const uint32_t o0 = __ldg(eptr + j), o1 = __ldg(eptr + j + 1), o2 = __ldg(eptr + j + 2);
+                        n0 = (int)((o1 - o0) / 6);
+                        n1 = (int)((o2 - o1) / 6);
                     }
-                    tc::mbar_wait(&efull[es], ephase);
-                    tc::mbar_wait(&empty[stage], phase ^ 1);
+                    tc::mbar_spin(&empty[stage], phase ^ 1);
                     uint8_t *a_s = ring + stage * L.slot_bytes;
-                    uint4 *z = reinterpret_cast<uint4 *>(a_s + h * (P_A / 2));
-#pragma unroll 4
-                    for (int i = lane; i < P_A / 2 / 16; i += 32) z[i] = make_uint4(0, 0, 0, 0);
+                    if (!(P.debug & 32)) {
+                        uint4 *z = reinterpret_cast<uint4 *>(a_s);
+#pragma unroll 8
+                        for (int i = lane; i < P_A / 16; i += 32) z[i] = make_uint4(0, 0, 0, 0);
+                    }
+                    tc::mbar_spin(&efull[es], ephase);
                     __syncwarp();
-                    const uint8_t *el = eslots + es * L.eslot_bytes + h * L.ehalf_bytes;
-                    const uint32_t *vals = reinterpret_cast<const uint32_t *>(el);
-                    const uint16_t *offs = reinterpret_cast<const uint16_t *>(el + 4 * n);
                     uint32_t *w32 = reinterpret_cast<uint32_t *>(a_s);
-                    for (int i = lane; i < n; i += 32) w32[offs[i]] = vals[i];
-                    tc::fence_proxy_async_smem();
+                    if (!(P.debug & 64)) {
+#pragma unroll 1
+                        for (int hh = 0; hh < 2; ++hh) {
+                            const int n = hh ? n1 : n0;
+                            const uint8_t *el = eslots + es * L.eslot_bytes + hh * L.ehalf_bytes;
+                            // 4 entries per lane per step: 16 B of values, 8 B of offsets
+                            const uint4 *v4 = reinterpret_cast<const uint4 *>(el);
+                            const uint2 *o4 = reinterpret_cast<const uint2 *>(el + 4 * n);
+                            for (int i = lane; i < n / 4; i += 32) {
+                                const uint4 v = v4[i];
+                                const uint2 o = o4[i];
+                                w32[o.x & 0xFFFF] = v.x;
+                                w32[o.x >> 16] = v.y;
+                                w32[o.y & 0xFFFF] = v.z;
+                                w32[o.y >> 16] = v.w;
+                            }
+                        }
+                    }
+                    if (!(P.debug & 128)) tc::fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
                         tc::mbar_arrive(&eempty[es]);
                         tc::mbar_arrive_cluster(full0 + 8 * stage);
                     }
-                    if (++es == ES) { es = 0; ephase ^= 1; }
-                    if (++stage == S) { stage = 0; phase ^= 1; }
                 }
             }
         }
@@ -980,11 +1026,12 @@ bool plan_xlayout(const SiImage *h, bool xstat, XLayout &L, int &smem)
     L.ehalf_bytes = ((h->tc_emax * 6 + 127) / 128) * 128;
     L.eslot_bytes = 2 * L.ehalf_bytes;
     const int fixed = 1024 + 1024 + L.xbytes + L.staged + L.tables;
-    for (int es = 4; es >= 2; --es) {
+    // deep entry ring first (bulk-copy latency ~2 us), then W slots (>= 3)
+    for (int es = X_MAXSLOTS; es >= 2; --es) {
         const int room = SMEM_MAX - fixed - es * L.eslot_bytes;
         int st = room / L.slot_bytes;
-        if (st > 6) st = 6;
-        if (st >= 2) {
+        if (st > 4) st = 4;
+        if (st >= 3 || (es == 2 && st >= 2)) {
             L.nstages = st;
             L.neslots = es;
             smem = fixed + es * L.eslot_bytes + st * L.slot_bytes;
@@ -1099,7 +1146,10 @@ int k2_launch(const SpmmArgs &a)
     }();
     // the pair kernels tile W rows by 256; an odd count of 128-row tiles reads
     // one tile of TMA out-of-bounds zero fill
-    int variant = forced >= 0 ? forced : (h->tc_kpad <= KMAX_XSTAT ? V_EXPAND_XSTAT : V_EXPAND);
+    // measured defaults ("K2 variants"): single CTA for K <= 1024,
+    // CTA pair beyond; the X-stationary and expanded-W variants are kept
+    // selectable for the ongoing tuning
+    int variant = forced >= 0 ? forced : (h->tc_kpad <= KMAX_XSTAT ? V_SINGLE : V_PAIR);
     if (variant == V_PAIR_XSTAT && h->tc_kpad > KMAX_XSTAT) variant = V_PAIR;
     if (variant == V_EXPAND_XSTAT && h->tc_kpad > KMAX_XSTAT) variant = V_EXPAND;
 
@@ -1130,6 +1180,14 @@ int k2_launch(const SpmmArgs &a)
     if (out32) {
         std::memset(&to, 0, sizeof(to));
         return launch_outk<OUT_32>(a, tw, tx, to, p, variant);
+    }
+    // 8-bit stores: TMA store of a swizzled smem tile (default; measured
+    // fastest) or quad-transposed direct 32-bit stores (SI_K2_STORE=direct)
+    static const bool use_direct = [] { const char *e = getenv("SI_K2_STORE"); return e && std::string(e) == "direct"; }();
+    if (use_direct && a.ldo % 4 == 0 && (uintptr_t)a.out % 4 == 0) {
+        std::memset(&to, 0, sizeof(to));
+        return h->out_dtype == 2 ? launch_outk<OUT_U8_Q>(a, tw, tx, to, p, variant)
+                                 : launch_outk<OUT_S8_Q>(a, tw, tx, to, p, variant);
     }
     const bool tma_ok = (a.ldo % 16 == 0) && ((uintptr_t)a.out % 16 == 0) &&
                         encode_2d(&to, a.out, (uint64_t)h->M, (uint64_t)a.n, (uint64_t)a.ldo, 128, COLS);

@@ -198,9 +198,12 @@ __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank)
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(saddr), "r"(rank));
     return d;
 }
+// arrive on a barrier of any CTA of the cluster.  Default (.release.cta)
+// semantics, as CUTLASS's 2-SM pipelines use: the .release.cluster form
+// compiles to MEMBAR.ALL.GPU per arrive, which dominated the expander loop.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr)
 {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t *b, uint32_t parity)
 {
