@@ -1,0 +1,24 @@
+#!/bin/bash
+# One GPU call: tests, smoke, bench, ncu launch list, ncu full capture of the
+# dominant kernel.  Outputs under gpurun_out/ (copied to profiles/ by
+# tools/summarize_profiles.py).  Each ncu step runs only after the same
+# command exited 0 without ncu.
+set -u
+cd "${GRAFT_REPO_ROOT:-$(pwd)}"
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > gpurun_out/gpu.txt 2>&1
+timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+CMD="python bench.py --steps 2 --warmup 3 --no-cpu --e2e-steps 1"
+if timeout 600 $CMD > gpurun_out/plain_launch.log 2>&1; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+     --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
+fi
+P1="python tests/prof_one.py c5b auto 3"
+if timeout 300 $P1 > gpurun_out/plain_prof.log 2>&1; then
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k2 -s 2 -c 1 \
+     -o gpurun_out/prof_top $P1 > gpurun_out/ncu_full.log 2>&1
+fi
+echo done
