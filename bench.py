@@ -255,7 +255,8 @@ def main():
     tp = os.path.join(ROOT, "profiles", "dram_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(dc.name)
+            t = json.load(f).get(dc.name)
+        traffic = None if t is None else int(t["per_launch_bytes"])
 
     # ---- e2e: public API with host buffers (pinned H2D of X, D2H of outputs)
     h2d = sum(L["x_host"].numel() for L in layers)
