@@ -72,7 +72,8 @@ struct SiImage {
     int32_t tc_nlists;       // tc_mtiles * kchunks * 2
     uint64_t off_tc_eptr;    // u32   [tc_nlists + 1]   byte offsets into the entry section
     uint64_t off_tc_ent;     // bytes                   entry lists
-    uint64_t reserved2;
+    uint64_t off_rqg;        // f32   [M]               per-row epilogue bound: < 0 if |acc+adj| may reach
+                             //                         2^22, else 2^-20 * max|r| (requant guard; 0 otherwise)
 };
 
 static_assert(sizeof(SiImage) % 16 == 0, "image header must stay 16-byte aligned");

@@ -265,7 +265,7 @@ Compiled compile_program(const si_program *p)
 }
 
 struct Layout {
-    uint64_t off[20];
+    uint64_t off[21];
     uint64_t total;
 };
 
@@ -423,6 +423,7 @@ static Layout make_layout(const si_weight *w, const si_program *p, const Compile
     put(17, 2 * c.bp_bucket.size());
     put(18, 4 * x.ptr.size());
     put(19, x.bytes.size());
+    put(20, 4 * M);
     l.total = cur;
     return l;
 }
@@ -471,6 +472,7 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
     h->bp_key_lo = c.bp_key_lo;
     h->bp_shift = c.bp_shift;
     h->bp_nbucket = (int32_t)c.bp_bucket.size();
+    h->off_rqg = l.off[20];
     h->off_tc_eptr = l.off[18];
     h->off_tc_ent = l.off[19];
     h->tc_emax = x.emax;
@@ -507,6 +509,35 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
         }
     }
     h->nnz_blocks = nnz;
+
+    // per-row bound on |acc + adj| (u8 activations <= 255): rows whose bound
+    // stays below 2^22 never leave the magic-number range, and for requant
+    // the certificate guard 2^-20 * max|r| becomes a per-row constant
+    {
+        float *rqg = (float *)(base + h->off_rqg);
+        for (int32_t g = 0; g < G; ++g) {
+            int64_t sabs[4] = {0, 0, 0, 0};
+            for (int64_t q = w->group_ptr[g]; q < w->group_ptr[g + 1]; ++q)
+                for (int r = 0; r < 4; ++r) {
+                    const int v = w->vals[(q / 4) * 16 + r * 4 + (q % 4)];
+                    sabs[r] += v < 0 ? -v : v;
+                }
+            for (int r = 0; r < 4; ++r) {
+                const int64_t m = (int64_t)g * 4 + r;
+                if (m >= M) break;
+                const int64_t a = adj[m] < 0 ? -(int64_t)adj[m] : (int64_t)adj[m];
+                const double bound = 255.0 * (double)sabs[r] + (double)a;
+                if (bound >= 4194304.0) {
+                    rqg[m] = -1.0f;
+                } else if (c.mode == EPI_REQUANT || c.mode == EPI_REQUANT_LUT) {
+                    const double cm = (double)p->scale_in[m] / (double)c.q_scale;
+                    rqg[m] = (float)(bound * (cm > 0 ? cm : -cm) * 9.5367431640625e-07 * (1.0 + 1.0 / 1024));
+                } else {
+                    rqg[m] = 0.0f;
+                }
+            }
+        }
+    }
 
     std::memcpy(base + h->off_scale_in, p->scale_in, 4 * (size_t)M);
     if (p->n_ops) {
