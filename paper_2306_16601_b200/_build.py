@@ -19,6 +19,9 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_native")
 LIB_NAME = "libsparseinfer_b200.so"
 LIB_PATH = os.path.join(OUT_DIR, LIB_NAME)
+# experiment builds: SI_BUILD_DEFS="-DNAME ..." -> a separate library that
+# SI_LIB=<path> selects at load time (never the default product library)
+EXTRA_DEFS = os.environ.get("SI_BUILD_DEFS", "").split()
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off",
@@ -34,7 +37,7 @@ def nvcc() -> str:
 
 
 def _compile(src: str, obj: str, log_dir: str) -> None:
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-I", os.path.join(HERE, "..", "include"), "-c",
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *EXTRA_DEFS, "-I", os.path.join(HERE, "..", "include"), "-c",
            os.path.join(CSRC, src), "-o", obj]
     if src.endswith(".cpp"):
         cmd.insert(1, "-x")
@@ -56,23 +59,25 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False) -> str:
+def build(force: bool = False, out: str | None = None) -> str:
     """Compile (if stale) and return the library path."""
-    if not force and not _stale():
+    lib_path = out or LIB_PATH
+    if not force and out is None and not _stale():
         return LIB_PATH
-    obj_dir = os.path.join(OUT_DIR, "obj")
+    obj_dir = os.path.join(OUT_DIR, "obj" if out is None else "obj_exp")
     os.makedirs(obj_dir, exist_ok=True)
     objs = [os.path.join(obj_dir, s.rsplit(".", 1)[0] + ".o") for s in SOURCES]
     with cf.ThreadPoolExecutor(len(SOURCES)) as ex:
         list(ex.map(lambda so: _compile(so[0], so[1], obj_dir), zip(SOURCES, objs)))
-    tmp = LIB_PATH + ".tmp"
+    tmp = lib_path + ".tmp"
     cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr[-4000:]}")
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":
-    print(build(force=True))
+    import sys
+    print(build(force=True, out=sys.argv[1] if len(sys.argv) > 1 else None))

@@ -45,7 +45,7 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB_PATH
+    path = os.environ.get("SI_LIB") or _build.LIB_PATH   # SI_LIB: experiment builds only
     if not os.path.exists(path):
         try:
             path = _build.build()

@@ -72,8 +72,20 @@ struct SiImage {
     int32_t tc_nlists;       // tc_mtiles * kchunks * 2
     uint64_t off_tc_eptr;    // u32   [tc_nlists + 1]   byte offsets into the entry section
     uint64_t off_tc_ent;     // bytes                   entry lists
-    uint64_t off_rqg;        // f32   [M]               per-row epilogue bound: < 0 if |acc+adj| may reach
-                             //                         2^22, else 2^-20 * max|r| (requant guard; 0 otherwise)
+    uint64_t off_rqg;        // f32   [M]               per-row epilogue class: -1 if |acc+adj| may reach 2^22,
+                             //                         1 requant rounding proven exact (plan.cpp
+                             //                         requant_row_exact), else the requant certificate
+                             //                         guard 2^-22 max|r| (<= 1/4; 0 for other modes)
+    // K2s (2:4 sparse tensor cores): per (128-row tile, 128-k chunk) a 12 KB
+    // image = compressed A [128 rows x 64 B] (K-major, SWIZZLE_NONE core
+    // matrices, LBO 128 / SBO 512) + two metadata tiles [128 rows x 16 B]
+    // (bytes 0-7: 4-bit idx0|idx1<<2 per 4-wide k window; SBO 128), and
+    // per-row residual lists for windows with > 2 nonzero columns.
+    uint64_t off_sp_img;     // bytes [even(tc_mtiles) * kchunks * 12288]
+    uint64_t off_sp_rptr;    // i32   [tc_mtiles * 128 + 1] residual entry offsets per padded row
+    uint64_t off_sp_res;     // i32   [n_res]  (k << 8) | (uint8)w
+    int32_t sp_nres, sp_maxres;  // residual entries, max per row
+    uint64_t reserved3, reserved4;
 };
 
 static_assert(sizeof(SiImage) % 16 == 0, "image header must stay 16-byte aligned");

@@ -265,7 +265,7 @@ Compiled compile_program(const si_program *p)
 }
 
 struct Layout {
-    uint64_t off[21];
+    uint64_t off[24];
     uint64_t total;
 };
 
@@ -277,6 +277,152 @@ struct ExpandLists {
     std::vector<uint8_t> bytes;
     int32_t emax = 0;
 };
+
+// True when the device's requant rounding, rint(RN32(f32(a) * c)) + zp
+// clamped to [lo, hi] with c = f32(s / fp), equals the reference's
+// rint((f64(a) * s) / fp) + zp clamped (epilogue.py:218-228) for every
+// integer |a| <= A.  Both rounded values are monotone in a, so they agree
+// everywhere iff every output step (k-1 -> k, lo-zp < k <= hi-zp) happens at
+// the same a; each step is located from the estimate (k - 1/2) / (s / fp)
+// by exact evaluation of both expressions.
+static bool requant_row_exact(int64_t A, float s_in, float fp, float c, int32_t zp, int32_t lo, int32_t hi)
+{
+    const double q = (double)s_in / (double)fp;
+    if (!(c != 0.0f) || !std::isfinite(c) || !std::isfinite(q) || q == 0.0) return false;
+    if ((double)A * std::fabs((double)c) >= 2097152.0) return false;   // |r| < 2^21: magic rint exact
+    const int64_t sg = c > 0 ? 1 : -1;
+    auto Rr = [&](int64_t t) {
+        const float af = (float)(sg * t);
+        const float r = af * c;
+        return (int64_t)std::nearbyint((double)r);
+    };
+    auto Ry = [&](int64_t t) {
+        const double y = ((double)(sg * t) * (double)s_in) / (double)fp;
+        return (int64_t)std::nearbyint(y);
+    };
+    auto step = [&](auto R, int64_t k, int64_t &out) {
+        // smallest t in [-A, A + 1] with R(t) >= k (A + 1: never)
+        double est = std::ceil(((double)k - 0.5) / std::fabs(q));
+        est = std::min(std::max(est, (double)-A), (double)(A + 1));
+        int64_t t = (int64_t)est;
+        int steps = 0;
+        while (t > -A && R(t - 1) >= k) { --t; if (++steps > 4096) return false; }
+        while (t <= A && R(t) < k) { ++t; if (++steps > 4096) return false; }
+        out = t;
+        return true;
+    };
+    for (int64_t k = (int64_t)lo - zp + 1; k <= (int64_t)hi - zp; ++k) {
+        int64_t tr = 0, ty = 0;
+        if (!step(Rr, k, tr) || !step(Ry, k, ty) || tr != ty) return false;
+    }
+    return true;
+}
+
+// K2s 2:4 images (see image.h).  A window (group, 4 consecutive k) keeps
+// its first two nonzero columns in the compressed operand; further columns
+// go to the per-row residual lists.
+struct SparseImages {
+    std::vector<uint8_t> img;
+    std::vector<int32_t> rptr;
+    std::vector<int32_t> res;
+    int32_t maxres = 0;
+};
+
+SparseImages build_sparse_images(const si_weight *w)
+{
+    SparseImages S;
+    const int32_t G = w->rows / 4;
+    const int32_t rt_n = (w->logical_rows + 127) / 128;
+    const int32_t kch = (w->cols + 127) / 128;
+    const int32_t rt_pad = (rt_n + 1) / 2 * 2;   // whole 256-row pair tiles
+    S.img.assign((size_t)rt_pad * kch * 12288, 0);
+    std::vector<std::vector<int32_t>> rres((size_t)rt_n * 128);
+    for (int32_t g = 0; g < G && g / 32 < rt_n; ++g) {
+        const int32_t rt = g / 32, gl = g % 32;
+        // dense 4-row strip of this group: column -> 4 values (summing duplicates, int8 wrap)
+        std::vector<std::pair<int32_t, uint32_t>> cols;
+        for (int64_t q = w->group_ptr[g]; q < w->group_ptr[g + 1]; ++q) {
+            uint32_t word = 0;
+            for (int r = 0; r < 4; ++r) {
+                uint8_t b = (uint8_t)w->vals[(q / 4) * 16 + r * 4 + (q % 4)];
+                if (g * 4 + r >= w->logical_rows) b = 0;
+                word |= (uint32_t)b << (8 * r);
+            }
+            if (!word) continue;
+            bool merged = false;
+            for (auto &c : cols)
+                if (c.first == w->idx[q]) {
+                    uint32_t sum = 0;
+                    for (int r = 0; r < 4; ++r)
+                        sum |= (uint32_t)(uint8_t)((int8_t)(c.second >> (8 * r)) + (int8_t)(word >> (8 * r))) << (8 * r);
+                    c.second = sum;
+                    merged = true;
+                    break;
+                }
+            if (!merged) cols.emplace_back(w->idx[q], word);
+        }
+        std::sort(cols.begin(), cols.end());
+        size_t i = 0;
+        while (i < cols.size()) {
+            const int32_t win = cols[i].first / 4;
+            size_t j = i;
+            while (j < cols.size() && cols[j].first / 4 == win) ++j;
+            const int32_t kc = win / 32, wl = win % 32;     // window within the 128-k chunk
+            uint8_t *tile = S.img.data() + ((size_t)rt * kch + kc) * 12288;
+            // slots: up to two kept columns, ascending window index
+            int32_t idx0 = 0, idx1 = 1;
+            uint32_t v0 = 0, v1 = 0;
+            const size_t kept = std::min<size_t>(2, j - i);
+            if (kept == 2) {
+                idx0 = cols[i].first % 4; v0 = cols[i].second;
+                idx1 = cols[i + 1].first % 4; v1 = cols[i + 1].second;
+            } else if (kept == 1) {
+                const int32_t ii = cols[i].first % 4;
+                if (ii == 3) { idx0 = 0; idx1 = 3; v1 = cols[i].second; }
+                else { idx0 = ii; idx1 = 3; v0 = cols[i].second; }
+            }
+            for (size_t e = i + kept; e < j; ++e)
+                for (int r = 0; r < 4; ++r) {
+                    const int8_t v = (int8_t)(cols[e].second >> (8 * r));
+                    if (v) rres[(size_t)rt * 128 + gl * 4 + r].push_back((cols[e].first << 8) | (uint8_t)v);
+                }
+            const int32_t mma = wl / 16, wm = wl % 16;        // MMA (64 logical k) and window in it
+            const uint8_t nib = (uint8_t)(idx0 | (idx1 << 2));
+            for (int r = 0; r < 4; ++r) {
+                const int32_t row = gl * 4 + r;
+                const int32_t pb0 = 2 * wl, pb1 = 2 * wl + 1;  // physical bytes of the window
+                auto aoff = [&](int32_t pb) {
+                    return (row / 8) * 512 + (pb / 16) * 128 + (row % 8) * 16 + (pb % 16);
+                };
+                tile[aoff(pb0)] = (uint8_t)(v0 >> (8 * r));
+                tile[aoff(pb1)] = (uint8_t)(v1 >> (8 * r));
+                uint8_t *e = tile + 8192 + mma * 2048 + (row / 8) * 128 + (row % 8) * 16 + wm / 2;
+                *e |= (wm % 2) ? (uint8_t)(nib << 4) : nib;
+            }
+            i = j;
+        }
+    }
+    // windows never touched keep metadata 0 = (idx 0, idx 0) over zero values:
+    // rewrite them to the canonical (0, 1)
+    for (size_t t = 0; t < (size_t)rt_pad * kch; ++t)
+        for (int mma = 0; mma < 2; ++mma)
+            for (int row = 0; row < 128; ++row) {
+                uint8_t *e = S.img.data() + t * 12288 + 8192 + mma * 2048 + (row / 8) * 128 + (row % 8) * 16;
+                for (int b = 0; b < 8; ++b)
+                    for (int h = 0; h < 2; ++h) {
+                        const uint8_t nib = (e[b] >> (4 * h)) & 0xF;
+                        if (nib == 0) e[b] |= (uint8_t)(0x4 << (4 * h));
+                    }
+            }
+    S.rptr.assign((size_t)rt_n * 128 + 1, 0);
+    for (size_t r = 0; r < rres.size(); ++r) {
+        S.rptr[r] = (int32_t)S.res.size();
+        S.maxres = std::max<int32_t>(S.maxres, (int32_t)rres[r].size());
+        S.res.insert(S.res.end(), rres[r].begin(), rres[r].end());
+    }
+    S.rptr[rres.size()] = (int32_t)S.res.size();
+    return S;
+}
 
 ExpandLists build_expand_lists(const si_weight *w)
 {
@@ -395,7 +541,8 @@ static int32_t validate(const si_weight *w, const si_program *p)
     return SI_OK;
 }
 
-static Layout make_layout(const si_weight *w, const si_program *p, const Compiled &c, const ExpandLists &x)
+static Layout make_layout(const si_weight *w, const si_program *p, const Compiled &c, const ExpandLists &x,
+                          const SparseImages &sp)
 {
     Layout l{};
     const int64_t G = w->rows / 4, T = w->group_ptr[G], tiles = T / 4;
@@ -424,6 +571,9 @@ static Layout make_layout(const si_weight *w, const si_program *p, const Compile
     put(18, 4 * x.ptr.size());
     put(19, x.bytes.size());
     put(20, 4 * M);
+    put(21, sp.img.size());
+    put(22, 4 * sp.rptr.size());
+    put(23, 4 * sp.res.size());
     l.total = cur;
     return l;
 }
@@ -434,7 +584,8 @@ extern "C" int32_t si_plan_image_size(const si_weight *w, const si_program *p, u
     if (rc) return rc;
     Compiled c = compile_program(p);
     ExpandLists x = build_expand_lists(w);
-    *bytes = make_layout(w, p, c, x).total;
+    SparseImages sp = build_sparse_images(w);
+    *bytes = make_layout(w, p, c, x, sp).total;
     return SI_OK;
 }
 
@@ -445,7 +596,8 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
     if (rc) return rc;
     Compiled c = compile_program(p);
     ExpandLists x = build_expand_lists(w);
-    Layout l = make_layout(w, p, c, x);
+    SparseImages sp = build_sparse_images(w);
+    Layout l = make_layout(w, p, c, x, sp);
     if (bytes < l.total) { si_set_error("image buffer too small"); return SI_ENOSPACE; }
     uint8_t *base = (uint8_t *)host_image;
     std::memset(base, 0, l.total);
@@ -473,6 +625,14 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
     h->bp_shift = c.bp_shift;
     h->bp_nbucket = (int32_t)c.bp_bucket.size();
     h->off_rqg = l.off[20];
+    h->off_sp_img = l.off[21];
+    h->off_sp_rptr = l.off[22];
+    h->off_sp_res = l.off[23];
+    h->sp_nres = (int32_t)sp.res.size();
+    h->sp_maxres = sp.maxres;
+    std::memcpy(base + h->off_sp_img, sp.img.data(), sp.img.size());
+    std::memcpy(base + h->off_sp_rptr, sp.rptr.data(), 4 * sp.rptr.size());
+    if (!sp.res.empty()) std::memcpy(base + h->off_sp_res, sp.res.data(), 4 * sp.res.size());
     h->off_tc_eptr = l.off[18];
     h->off_tc_ent = l.off[19];
     h->tc_emax = x.emax;
@@ -511,8 +671,11 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
     h->nnz_blocks = nnz;
 
     // per-row bound on |acc + adj| (u8 activations <= 255): rows whose bound
-    // stays below 2^22 never leave the magic-number range, and for requant
-    // the certificate guard 2^-20 * max|r| becomes a per-row constant
+    // stays below 2^22 never leave the magic-number range (rqg >= 0).  For
+    // requant, rows where the f32 rounding provably matches the reference's
+    // f64 rounding for every reachable accumulator get rqg = 1 (no
+    // certificate); the other rows get the certificate guard 2^-22 * max|r|
+    // as a per-row constant (0 <= rqg <= 1/4).
     {
         float *rqg = (float *)(base + h->off_rqg);
         for (int32_t g = 0; g < G; ++g) {
@@ -526,12 +689,18 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
                 const int64_t m = (int64_t)g * 4 + r;
                 if (m >= M) break;
                 const int64_t a = adj[m] < 0 ? -(int64_t)adj[m] : (int64_t)adj[m];
-                const double bound = 255.0 * (double)sabs[r] + (double)a;
-                if (bound >= 4194304.0) {
+                const int64_t bound = 255 * sabs[r] + a;
+                if (bound >= 4194304) {
                     rqg[m] = -1.0f;
-                } else if (c.mode == EPI_REQUANT || c.mode == EPI_REQUANT_LUT) {
-                    const double cm = (double)p->scale_in[m] / (double)c.q_scale;
-                    rqg[m] = (float)(bound * (cm > 0 ? cm : -cm) * 9.5367431640625e-07 * (1.0 + 1.0 / 1024));
+                } else if (c.mode == EPI_REQUANT) {
+                    const float cm = (float)((double)p->scale_in[m] / (double)c.q_scale);
+                    if (requant_row_exact(bound, p->scale_in[m], c.q_scale, cm, c.q_zp, c.q_lo, c.q_hi)) {
+                        rqg[m] = 1.0f;
+                    } else {
+                        // certificate guard 2^-22 * max|r| (max|r| <= bound * |c|), rounded up
+                        const double g = (double)bound * std::fabs((double)cm) * 2.384185791015625e-07 * (1.0 + 1.0 / 1024);
+                        rqg[m] = (float)std::min(g * (1.0 + 1e-6) + 1e-30, 0.25);
+                    }
                 } else {
                     rqg[m] = 0.0f;
                 }

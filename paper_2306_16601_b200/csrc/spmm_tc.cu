@@ -8,23 +8,27 @@
 // so no relayout pass exists.  Integer MACs are exact and wrap mod 2^32, so
 // the expansion changes no bit of the accumulator.
 //
-// Two kernels share one epilogue:
+// Kernels sharing one epilogue:
 //
-//  k2p  (default) a CTA *pair* (cluster of 2, tcgen05 cta_group::2).  The
-//       pair computes D[256 W rows x 256 tokens] per MMA tile; each CTA
-//       holds half of A (128 W rows) and half of B (128 tokens) in its smem,
-//       so every SM moves half the operand bytes a single CTA would.  With
-//       K <= 1024 the pair's activation tile stays resident in smem
-//       ("X-stationary") while W streams through the ring, so X is read
-//       from HBM once and only W^T (L2-resident) is re-streamed.
-//  k2   single CTA, M128 x N256 tiles, both operands streamed (kept as the
-//       A/B reference; SI_K2_VARIANT=single selects it).
+//  k2   single CTA, M128 x N256 tiles, both operands streamed through a TMA
+//       ring (default for K <= 1024).
+//  k2p  a CTA *pair* (cluster of 2, tcgen05 cta_group::2) computing
+//       D[256 W rows x 256 tokens] per tile; each CTA holds half of A and
+//       half of B, so every SM moves half the operand bytes (default for
+//       K > 1024).  XSTAT keeps the pair's activation tile resident while W
+//       streams (SI_K2_VARIANT=xstat).
+//  k2x  pair + expander warps that build the dense W tile in smem from the
+//       block lists (SI_K2_VARIANT=expand[_xstat]).
+//  k2s  pair on the 2:4 sparse tensor-core path (tcgen05.mma.sp): the plan
+//       packs each 4-wide k window's first two nonzero columns into the
+//       compressed operand + metadata; columns beyond two per window are
+//       added in the epilogue from per-row residual lists.  M256 x N192
+//       tiles so the metadata fits TMEM next to two accumulators.
 //
-// Roles (both kernels): warp 0 TMA producer, warp 1 TMEM allocator + MMA
-// issuer (one thread; in the pair only the leader CTA issues), warps 2..17
-// epilogue (16 warps, 4 per TMEM lane quarter, 64 tokens each).  TMEM holds
-// two 256-column s32 accumulators so the epilogue of tile i overlaps the
-// MMAs of tile i+1.
+// Roles: warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer (one
+// thread; in a pair only the leader CTA issues), then the epilogue warps (4
+// per TMEM lane quarter, 64 tokens each).  TMEM holds two accumulators so the
+// epilogue of tile i overlaps the MMAs of tile i+1.
 //
 // Epilogue (all compiled forms of the reference's _run_chain,
 // epilogue.py:207-249): tcgen05.ld 32x32b.x32 -> registers -> the form's
@@ -34,12 +38,12 @@
 // run on the quarter-rate XU pipe): the accumulator becomes an f32 by the
 // 1.5*2^23 magic-number trick (exact for |a| < 2^22), r = a * c[m] with
 // c = f32(scale_in/fp) in packed f32x2 ops, rint(r) by the same magic, and
-// the certificate |r - rint(r)| + 2^-20|r| < 1/2 is max-reduced per 32
+// the certificate |r - rint(r)| + 2^-22|r| < 1/2 is max-reduced per 32
 // elements; a chunk that fails it (or holds an out-of-range accumulator)
 // recomputes the flagged elements with the reference's f64 expression.
-// Error bound: |r - y| <= 3 * 2^-24 |y| (one rounding each for a, c, a*c;
-// y = the reference's f64 value), so outside the certificate's band rint(r)
-// == rint(y) and the output bits match.
+// Error bound: |r - y| <= (2^-23 + 2^-48)|y| (a exact, one rounding each for
+// c and a*c; y = the reference's f64 value), so outside the certificate's
+// band rint(r) == rint(y) and the output bits match.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -61,6 +65,16 @@ constexpr int EPI_GROUPS = EPI_WARPS / 4;   // token column groups
 constexpr int TILE_N = 256;                 // tokens per accumulator tile
 constexpr int COLS = TILE_N / EPI_GROUPS;   // tokens per epilogue warp (64)
 constexpr int THREADS = 32 * (2 + EPI_WARPS);
+// TMA issue: one issuing warp sustains about one box per ~200 ns (tools/
+// tma_bw.py), so the single/pair/sparse kernels spread their loads over
+// NPROD producer warps (warp 0 + NPROD-1 warps after the epilogue warps),
+// producer p taking the ring iterations it == p (mod NPROD)
+constexpr int NPROD = 3;   // 20 warps: keeps the 96-register cap (warps allocate in groups of 4)
+constexpr int MT_THREADS = THREADS + 32 * (NPROD - 1);
+__device__ __forceinline__ int producer_index(int warp, int first_extra)
+{
+    return warp == 0 ? 0 : (warp >= first_extra && warp < first_extra + NPROD - 1) ? warp - first_extra + 1 : -1;
+}
 constexpr int STG_GROUP = 128 * COLS;       // staging bytes per column group (8-bit outputs)
 constexpr int STG_BYTES = EPI_GROUPS * STG_GROUP;
 constexpr int TABLE_BYTES = 16 * 1024;      // breakpoint tables staged in smem (EPI_DEQ_TABLE)
@@ -80,6 +94,10 @@ struct K2Params {
     const float *rqc;    // requant c[m] = f32(scale_in[m] / fp)
     const float *rqg;    // per-row bound (image off_rqg): < 0 unsafe, else requant guard
     int32_t rtiles;      // 128-row weight tiles with expansion lists (k2x)
+    const uint8_t *x;    // K2s residual: activations [K][ldx] (KN layout)
+    int64_t ldx;
+    const int32_t *sp_rptr;  // K2s residual entry offsets per padded row
+    const int32_t *sp_res;   // K2s residual entries (k << 8) | (uint8)w
     int32_t debug;       // experiment switches (SI_K2_DEBUG): 1 skip epilogue, 2 W tile 0 only,
                          // 4 X tile 0 only, 8 no TMA, 16 no MMA
 };
@@ -124,14 +142,41 @@ struct EpiWarp {
 // One 32-token chunk of one warp: TMEM columns -> outputs.  m is this
 // lane's weight row, n0 the chunk's first token, c the chunk index within the
 // warp's 64 columns (staging row offset).
-template <int MODE, int OUTK>
+template <int MODE, int OUTK, bool RES = false>
 __device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, int32_t adj, float s_in, float cq,
                                           float gm, bool fast, int64_t n0, int c, const K2Params &P,
-                                          const EpiParams &E, const EpiWarp &W)
+                                          const EpiParams &E, const EpiWarp &W, int32_t rp0 = 0, int32_t rp1 = 0)
 {
     uint32_t r[32];
     tc::tmem_ld_32x32b_x32(taddr, r);
     tc::tmem_ld_wait();
+    if constexpr (RES) {
+        // K2s: block columns that did not fit the 2:4 operand (windows with
+        // more than two nonzero columns), w * X[k][n0 .. n0+31] per entry
+#pragma unroll 1
+        for (int32_t e = rp0; e < ((P.debug & 512) ? rp0 : rp1); ++e) {
+            const int32_t ent = __ldg(P.sp_res + e);
+            const uint32_t w = (uint32_t)(int32_t)(int8_t)(ent & 0xFF);
+            const uint8_t *xp = P.x + (int64_t)(ent >> 8) * P.ldx + n0;
+            uint32_t xw[8];
+            if (n0 + 32 <= P.N) {
+                const uint4 a0 = __ldg(reinterpret_cast<const uint4 *>(xp));
+                const uint4 a1 = __ldg(reinterpret_cast<const uint4 *>(xp) + 1);
+                xw[0] = a0.x; xw[1] = a0.y; xw[2] = a0.z; xw[3] = a0.w;
+                xw[4] = a1.x; xw[5] = a1.y; xw[6] = a1.z; xw[7] = a1.w;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    xw[i] = 0;
+#pragma unroll
+                    for (int b = 0; b < 4; ++b)
+                        if (n0 + 4 * i + b < P.N) xw[i] |= (uint32_t)xp[4 * i + b] << (8 * b);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) r[j] += w * ((xw[j >> 2] >> (8 * (j & 3))) & 0xFFu);
+        }
+    }
     int32_t v[32];
     if constexpr (MODE == EPI_REQUANT) {
         const int32_t adjM = (int32_t)((uint32_t)adj + (uint32_t)MAGIC_I);
@@ -139,9 +184,23 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, i
         float emax = 0.0f;
         uint32_t umax = 0;
         const unsigned long long M2 = tc::f2pack(MAGIC_F, MAGIC_F), C2 = tc::f2pack(cq, cq);
-        if (fast) {
+        if (gm >= 1.0f) {   // (warp-uniform: all rows proven)
+            // every row of this warp is proven at plan time (requant_row_exact):
+            // the f32 rounding equals the reference's for all reachable accumulators
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+                const int32_t b0 = (int32_t)(r[j] + (uint32_t)adjM);
+                const int32_t b1 = (int32_t)(r[j + 1] + (uint32_t)adjM);
+                const unsigned long long af = tc::sub_f32x2(tc::f2pack(__int_as_float(b0), __int_as_float(b1)), M2);
+                const unsigned long long uu = tc::add_f32x2(tc::mul_f32x2(af, C2), M2);
+                v[j] = __float_as_int(tc::f2lo(uu)) - qoff;
+                v[j + 1] = __float_as_int(tc::f2hi(uu)) - qoff;
+            }
+        } else if (fast) {
             // every row of this warp provably stays within the magic-number
-            // range (plan-time bound 255*sum|w| + |adj| < 2^22): no range check
+            // range (plan-time bound 255*sum|w| + |adj| < 2^22) and |r| <= the
+            // row's max|r|: the certificate |d| + 2^-22|r| < 1/2 reduces to
+            // max|d| < 1/2 - guard (guard = 2^-22 max|r|, rqg; proven rows 0)
 #pragma unroll
             for (int j = 0; j < 32; j += 2) {
                 const int32_t b0 = (int32_t)(r[j] + (uint32_t)adjM);
@@ -150,11 +209,11 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, i
                 const unsigned long long rf = tc::mul_f32x2(af, C2);
                 const unsigned long long uu = tc::add_f32x2(rf, M2);
                 const unsigned long long d = tc::sub_f32x2(rf, tc::sub_f32x2(uu, M2));
-                emax = fmaxf(emax, __fmaf_rn(fabsf(tc::f2lo(rf)), CERT_G, fabsf(tc::f2lo(d))));
-                emax = fmaxf(emax, __fmaf_rn(fabsf(tc::f2hi(rf)), CERT_G, fabsf(tc::f2hi(d))));
+                emax = fmaxf(emax, fmaxf(fabsf(tc::f2lo(d)), fabsf(tc::f2hi(d))));
                 v[j] = __float_as_int(tc::f2lo(uu)) - qoff;
                 v[j + 1] = __float_as_int(tc::f2hi(uu)) - qoff;
             }
+            emax += gm;
         } else
 #pragma unroll
         for (int j = 0; j < 32; j += 2) {
@@ -290,7 +349,7 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, i
 // followed by the release of the accumulator and (8-bit) the TMA store of
 // the group's staging tile.  row0 = first weight row of this CTA's 128-row
 // half, tmem_col = accumulator column base.  release(): arrive on tempty.
-template <int MODE, int OUTK, typename Wait, typename Release>
+template <int MODE, int OUTK, bool RES = false, typename Wait, typename Release>
 __device__ __forceinline__ void epi_tile(uint32_t tmem_base, uint32_t tmem_col, int32_t row0, int64_t tok0,
                                          const CUtensorMap *tmap_o, const K2Params &P, const EpiParams &E,
                                          const EpiWarp &W, Wait wait_full, Release release)
@@ -303,8 +362,16 @@ __device__ __forceinline__ void epi_tile(uint32_t tmem_base, uint32_t tmem_col, 
     const float s_in = mok ? __ldg(E.scale_in + m) : 0.0f;
     float cq = 0.0f;
     if (MODE == EPI_REQUANT) cq = mok ? __ldg(P.rqc + m) : 0.0f;
-    const float gm = mok ? __ldg(P.rqg + m) : 0.0f;
-    const bool fast = !(P.debug & 256) && __all_sync(0xffffffffu, gm >= 0.0f);
+    const float gr = mok ? __ldg(P.rqg + m) : 1.0f;
+    const bool fast = !(P.debug & 256) && __all_sync(0xffffffffu, gr >= 0.0f);
+    // gm: 1 when every row of the warp is proven exact (no certificate), else
+    // this row's certificate guard (proven rows: 0)
+    const bool proven = !(P.debug & 256) && __all_sync(0xffffffffu, gr >= 1.0f);
+    const float gm = proven ? 1.0f : (gr >= 1.0f ? 0.0f : fmaxf(gr, 0.0f));
+    int32_t rp0 = 0, rp1 = 0;
+    if constexpr (RES) {
+        if (mok) { rp0 = __ldg(P.sp_rptr + m); rp1 = __ldg(P.sp_rptr + m + 1); }
+    }
     wait_full();
     tc::tc_fence_after();
     if constexpr (STAGED) {
@@ -316,8 +383,8 @@ __device__ __forceinline__ void epi_tile(uint32_t tmem_base, uint32_t tmem_col, 
 #pragma unroll 1
         for (int c = 0; c < COLS / 32; ++c) {
             const int col = W.g * COLS + c * 32;
-            epi_chunk<MODE, OUTK>(tmem_base + ((uint32_t)(W.q * 32) << 16) + tmem_col + col, m, mok, adj, s_in, cq,
-                                  gm, fast, tok0 + col, c, P, E, W);
+            epi_chunk<MODE, OUTK, RES>(tmem_base + ((uint32_t)(W.q * 32) << 16) + tmem_col + col, m, mok, adj, s_in,
+                                       cq, gm, fast, tok0 + col, c, P, E, W, rp0, rp1);
         }
     }
     // this warp's TMEM reads are complete: release the accumulator
@@ -334,7 +401,7 @@ __device__ __forceinline__ void epi_tile(uint32_t tmem_base, uint32_t tmem_col, 
     }
 }
 
-template <int MODE>
+template <int MODE, int NEPI = EPI_WARPS>
 __device__ __forceinline__ EpiWarp make_epi_warp(int warp, int lane, uint8_t *staging, uint8_t *tables,
                                                  const EpiParams &E)
 {
@@ -352,10 +419,10 @@ __device__ __forceinline__ EpiWarp make_epi_warp(int warp, int lane, uint8_t *st
     uint16_t *s_bkt = reinterpret_cast<uint16_t *>(tables + 8 * E.n_bp + 4);
     if constexpr (MODE == EPI_DEQ_TABLE) {
         const int et = threadIdx.x - 64;
-        for (int i = et; i < E.n_bp; i += 32 * EPI_WARPS) s_key[i] = __ldg(E.bp_key + i);
-        for (int i = et; i <= E.n_bp; i += 32 * EPI_WARPS) s_val[i] = __ldg(E.bp_v + i);
-        for (int i = et; i < E.bp_nbucket; i += 32 * EPI_WARPS) s_bkt[i] = __ldg(E.bp_bucket + i);
-        tc::named_bar_sync(1 + EPI_GROUPS, 32 * EPI_WARPS);
+        for (int i = et; i < E.n_bp; i += 32 * NEPI) s_key[i] = __ldg(E.bp_key + i);
+        for (int i = et; i <= E.n_bp; i += 32 * NEPI) s_val[i] = __ldg(E.bp_v + i);
+        for (int i = et; i < E.bp_nbucket; i += 32 * NEPI) s_bkt[i] = __ldg(E.bp_bucket + i);
+        tc::named_bar_sync(1 + EPI_GROUPS, 32 * NEPI);
     }
     W.s_key = s_key;
     W.s_val = s_val;
@@ -388,7 +455,7 @@ constexpr int single_smem()
 }
 
 template <int MODE, int OUTK>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(MT_THREADS, 1)
 k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
              const __grid_constant__ CUtensorMap tmap_o, const K2Params P, const EpiParams E)
 {
@@ -425,13 +492,19 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
     tc::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp == 0) {
+    const int prod = producer_index(warp, 2 + EPI_WARPS);
+    const int nprod = (P.debug & 4096) ? 1 : NPROD;   // 4096: single producer (A/B)
+    if (prod >= 0) {
         if (lane == 0) {
-            int stage = 0;
+            int stage = 0, it = 0;
             uint32_t phase = 0;
             for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
                 const int mt = tile % P.mtiles, nt = tile / P.mtiles;
-                for (int kc = 0; kc < P.kchunks; ++kc) {
+                for (int kc = 0; kc < P.kchunks; ++kc, ++it) {
+                    if (it % nprod != prod) {
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
                     tc::mbar_spin(&empty[stage], phase ^ 1);
                     uint8_t *a_s = smem + stage * S_STAGE;
                     uint8_t *b_s = a_s + S_A;
@@ -481,7 +554,7 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
                 if (acc == 0) acc_phase ^= 1;
             }
         }
-    } else {
+    } else if (warp < 2 + EPI_WARPS) {
         const EpiWarp W = make_epi_warp<MODE>(warp, lane, staging, tables, E);
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -528,7 +601,7 @@ constexpr int pair_smem()
 }
 
 template <int MODE, int OUTK, bool XSTAT>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MT_THREADS, 1)
 k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
            const __grid_constant__ CUtensorMap tmap_o, const K2Params P, const EpiParams E)
 {
@@ -593,19 +666,25 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
         }
     };
 
-    if (warp == 0) {
+    const int prod = producer_index(warp, 2 + EPI_WARPS);
+    const int nprod = (P.debug & 4096) ? 1 : NPROD;   // 4096: single producer (A/B)
+    if (prod >= 0) {
         if (lane == 0) {
-            // ---------------- TMA producer (both CTAs; bytes land on the leader's barriers)
+            // ---------------- TMA producers (both CTAs; bytes land on the leader's barriers)
             const uint32_t full0 = tc::mapa(tc::smem_u32(full), 0);
             const uint32_t xfull0 = tc::mapa(tc::smem_u32(xfull), 0);
-            int stage = 0;
+            int stage = 0, it = 0;
             uint32_t phase = 0, xphase = 0;
             for (int unit = pair; unit < units; unit += npairs) {
                 int nt, m_lo, m_hi;
                 unit_range(unit, nt, m_lo, m_hi);
                 const int tok = nt * TILE_N + 128 * (int)rank;
                 for (int mt = m_lo; mt < m_hi; ++mt) {
-                    for (int kc = 0; kc < P.kchunks; ++kc) {
+                    for (int kc = 0; kc < P.kchunks; ++kc, ++it) {
+                        if (it % nprod != prod) {
+                            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                            continue;
+                        }
                         if (XSTAT && mt == m_lo) {
                             // roll the resident X tile chunk by chunk: chunk kc is
                             // reloaded as soon as the previous unit's last MMA on it retires
@@ -670,7 +749,7 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
                 xphase ^= 1;
             }
         }
-    } else {
+    } else if (warp < 2 + EPI_WARPS) {
         // ---------------- epilogue warps (both CTAs; each reads its own TMEM half)
         const EpiWarp W = make_epi_warp<MODE>(warp, lane, staging, tables, E);
         const uint32_t tempty0 = tc::mapa(tc::smem_u32(tempty), 0);
@@ -689,6 +768,174 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }
+        }
+        if ((OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA) && W.q == 2 && lane == 0) tc::tma_store_wait_all0();
+    }
+    tc::tc_fence_before();
+    tc::cluster_sync();
+    if (warp == 1) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc_2sm(tmem_base, 512);
+    }
+}
+
+
+// ================================================================ clusters of CTA pairs sharing X
+// XM pairs (cluster of 2*XM CTAs) compute the same 256-token tile for XM
+// consecutive 256-row tiles.  Every CTA loads its own W half (2SM TMA, to its
+// pair leader's barrier) and a 128/XM-row k-slice of its token half of X,
+// multicast to the CTAs holding the same token half in all XM pairs: the
+// L2 -> crossbar traffic for X drops by XM (the pair kernel's TMA-only
+// mainloop runs at the lts2xbar peak, profiles/).  A non-leader CTA's X
+// slices complete on its own barrier; its warp 1 (idle there) forwards the
+// completion to the pair leader.  A stage is free again once all XM pair
+// leaders committed it (empty barrier count XM, commit multicast to the cluster).
+template <int MODE, int OUTK, int XM>
+constexpr int mc_stages()
+{
+    constexpr int s = (SMEM_MAX - staged_bytes<OUTK>() - table_bytes<MODE>() - 2048) / (P_A + P_B);
+    return s > 8 ? 8 : s;
+}
+template <int MODE, int OUTK, int XM>
+constexpr int mc_smem()
+{
+    return mc_stages<MODE, OUTK, XM>() * (P_A + P_B) + staged_bytes<OUTK>() + table_bytes<MODE>() + 1024 + 512;
+}
+
+template <int MODE, int OUTK, int XM>
+__global__ void __cluster_dims__(2 * XM, 1, 1) __launch_bounds__(MT_THREADS, 1)
+k2m_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
+           const __grid_constant__ CUtensorMap tmap_o, const K2Params P, const EpiParams E)
+{
+    constexpr int STAGES = mc_stages<MODE, OUTK, XM>();
+    constexpr int SLOT = P_A + P_B;
+    constexpr int XROWS = BK / XM;                   // k rows of each X slice
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
+    uint8_t *ring = smem;
+    uint8_t *staging = ring + STAGES * SLOT;
+    uint8_t *tables = staging + staged_bytes<OUTK>();
+    uint64_t *full = reinterpret_cast<uint64_t *>(tables + table_bytes<MODE>());
+    uint64_t *empty = full + STAGES;
+    uint64_t *tfull = empty + STAGES;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t crank = tc::cluster_ctarank();
+    const uint32_t q = crank >> 1, r = crank & 1, lead = 2 * q;
+    const int cl = blockIdx.x / (2 * XM), ncl = gridDim.x / (2 * XM);
+    const int mgroups = P.mtiles / XM;
+    const int units = P.ntiles * mgroups;
+    const uint16_t pair_mask = (uint16_t)(3u << lead);
+    const uint16_t all_mask = (uint16_t)((1u << (2 * XM)) - 1);
+    uint16_t xmask = 0;
+#pragma unroll
+    for (int i = 0; i < XM; ++i) xmask |= (uint16_t)(1u << (2 * i + r));
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            // leader: its producer's arrive.expect_tx + the peer's forward; peer: its producer
+            tc::mbar_init(&full[s], r == 0 ? 2 : 1);
+            tc::mbar_init(&empty[s], XM);
+        }
+        for (int a = 0; a < 2; ++a) {
+            tc::mbar_init(&tfull[a], 1);
+            tc::mbar_init(&tempty[a], 2 * EPI_WARPS);
+        }
+        tc::mbar_fence_init();
+        tc::tma_prefetch_desc(&tmap_w);
+        tc::tma_prefetch_desc(&tmap_x);
+    }
+    if (warp == 1) tc::tmem_alloc_2sm(tmem_slot, 512);
+    tc::tc_fence_before();
+    tc::cluster_sync();
+    tc::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int prod = producer_index(warp, 2 + EPI_WARPS);
+    const int nprod = (P.debug & 4096) ? 1 : NPROD;   // 4096: single producer (A/B)
+    if (prod >= 0) {
+        if (lane == 0) {
+            // ---------------- TMA producers
+            const uint32_t full_lead = tc::mapa(tc::smem_u32(full), lead);
+            int stage = 0, it = 0;
+            uint32_t phase = 0;
+            for (int unit = cl; unit < units; unit += ncl) {
+                const int nt = unit / mgroups, mt = (unit % mgroups) * XM + (int)q;
+                const int tok = nt * TILE_N + 128 * (int)r;
+                for (int kc = 0; kc < P.kchunks; ++kc, ++it) {
+                    if (it % nprod != prod) {
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
+                    tc::mbar_spin(&empty[stage], phase ^ 1);
+                    uint8_t *a_s = ring + stage * SLOT;
+                    // leader barrier: both W halves + its X half; peer barrier: its X half
+                    tc::mbar_expect_tx(&full[stage], r == 0 ? 2 * P_A + P_B : P_B);
+                    tc::tma_load_2d_2sm(a_s, &tmap_w, full_lead + 8 * stage, mt * 256 + 128 * (int)r, kc * BK);
+                    tc::tma_load_2d_mc(a_s + P_A + q * XROWS * 128, &tmap_x, &full[stage], tok,
+                                       kc * BK + (int)q * XROWS, xmask);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && r == 0) {
+            // ---------------- MMA issuer: pair leader, one thread, M256 x N256 x K32
+            const uint32_t idesc = tc::idesc_i8(256, TILE_N, 1, 1);
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, acc_phase = 0;
+            for (int unit = cl; unit < units; unit += ncl) {
+                tc::mbar_spin(&tempty[acc], acc_phase ^ 1);
+                tc::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * TILE_N;
+                for (int kc = 0; kc < P.kchunks; ++kc) {
+                    tc::mbar_spin(&full[stage], phase);
+                    tc::tc_fence_after();
+                    const uint32_t a_addr = tc::smem_u32(ring + stage * SLOT);
+                    const uint32_t b_addr = a_addr + P_A;
+#pragma unroll
+                    for (int kk = 0; kk < ((P.debug & 16) ? 0 : BK / 32); ++kk) {
+                        const uint64_t adesc = tc::smem_desc_sw128(a_addr + kk * 4096, P_A, 1024);
+                        const uint64_t bdesc = tc::smem_desc_sw128(b_addr + kk * 4096, P_B, 1024);
+                        tc::mma_i8_2sm(d_tmem, adesc, bdesc, idesc, (kc | kk) ? 1u : 0u);
+                    }
+                    tc::mma_commit_2sm_mc(&empty[stage], all_mask);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                tc::mma_commit_2sm_mc(&tfull[acc], pair_mask);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        } else if (lane == 0) {
+            // ---------------- peer CTA: forward X-slice completion to the pair leader
+            const uint32_t full_lead = tc::mapa(tc::smem_u32(full), lead);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int unit = cl; unit < units; unit += ncl) {
+                for (int kc = 0; kc < P.kchunks; ++kc) {
+                    tc::mbar_spin(&full[stage], phase);
+                    tc::mbar_arrive_cluster(full_lead + 8 * stage);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp < 2 + EPI_WARPS) {
+        // ---------------- epilogue warps (each CTA reads its own TMEM half)
+        const EpiWarp W = make_epi_warp<MODE>(warp, lane, staging, tables, E);
+        const uint32_t tempty_lead = tc::mapa(tc::smem_u32(tempty), lead);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int unit = cl; unit < units; unit += ncl) {
+            const int nt = unit / mgroups, mt = (unit % mgroups) * XM + (int)q;
+            const uint32_t te = tempty_lead + 8 * acc;
+            uint64_t *tf = &tfull[acc];
+            const uint32_t ph = acc_phase;
+            epi_tile<MODE, OUTK>(tmem_base, acc * TILE_N, mt * 256 + 128 * (int)r, (int64_t)nt * TILE_N, &tmap_o, P,
+                                 E, W, [tf, ph] { tc::mbar_wait(tf, ph); }, [te] { tc::mbar_arrive_cluster(te); });
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
         }
         if ((OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA) && W.q == 2 && lane == 0) tc::tma_store_wait_all0();
     }
@@ -973,6 +1220,176 @@ k2x_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ C
     }
 }
 
+// ================================================================ CTA pair, 2:4 sparse A
+// Per CTA and k chunk: the plan's 12 KB image of its 128 W rows (compressed
+// A 8 KB, K-major SWIZZLE_NONE, + two 2 KB metadata tiles) and 96 tokens x
+// 128 k of X as three SWIZZLE_32B atoms (32 tokens wide).  Per stage the
+// leader copies both metadata tiles into TMEM (tcgen05.cp, 4 columns each)
+// and issues two M256 x N192 x K64 tcgen05.mma.sp.  TMEM: accumulators at
+// columns [0,192) and [192,384), metadata slots at 384 and 392 (alternating
+// stages).
+constexpr int SP_TILE_N = 192;
+constexpr int SP_EPI_WARPS = 12;
+constexpr int SP_THREADS = 32 * (2 + SP_EPI_WARPS + NPROD - 1);
+constexpr int SP_IMG = 12288;
+constexpr int SP_BATOM = 32 * BK;          // 32 tokens x 128 k = 4 KB
+#ifdef SP_XEXP
+constexpr int SP_B = 4 * SP_BATOM;
+#else
+constexpr int SP_B = 3 * SP_BATOM;
+#endif
+constexpr int SP_SLOT = SP_IMG + SP_B;     // 24 KB
+constexpr uint32_t SP_ECOL = 2 * SP_TILE_N;
+
+template <int OUTK>
+constexpr int sp_staged() { return (OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA) ? 3 * STG_GROUP : 0; }
+template <int MODE, int OUTK>
+constexpr int sp_stages()
+{
+    constexpr int s = (SMEM_MAX - sp_staged<OUTK>() - table_bytes<MODE>() - 2048) / SP_SLOT;
+    return s > 8 ? 8 : s;
+}
+template <int MODE, int OUTK>
+constexpr int sp_smem()
+{
+    return sp_stages<MODE, OUTK>() * SP_SLOT + sp_staged<OUTK>() + table_bytes<MODE>() + 1024 + 512;
+}
+
+template <int MODE, int OUTK>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(SP_THREADS, 1)
+k2s_kernel(const __grid_constant__ CUtensorMap tmap_s, const __grid_constant__ CUtensorMap tmap_x,
+           const __grid_constant__ CUtensorMap tmap_o, const K2Params P, const EpiParams E)
+{
+    constexpr int STAGES = sp_stages<MODE, OUTK>();
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
+    uint8_t *ring = smem;
+    uint8_t *staging = ring + STAGES * SP_SLOT;
+    uint8_t *tables = staging + sp_staged<OUTK>();
+    uint64_t *full = reinterpret_cast<uint64_t *>(tables + table_bytes<MODE>());
+    uint64_t *empty = full + STAGES;
+    uint64_t *tfull = empty + STAGES;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = tc::cluster_ctarank();
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int units = P.ntiles * P.mtiles;          // (token tile, 256-row tile), rows fastest
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            tc::mbar_init(&tfull[a], 1);
+            tc::mbar_init(&tempty[a], 2 * SP_EPI_WARPS);
+        }
+        tc::mbar_fence_init();
+        tc::tma_prefetch_desc(&tmap_s);
+        tc::tma_prefetch_desc(&tmap_x);
+    }
+    if (warp == 1) tc::tmem_alloc_2sm(tmem_slot, 512);
+    tc::tc_fence_before();
+    tc::cluster_sync();
+    tc::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int prod = producer_index(warp, 2 + SP_EPI_WARPS);
+    const int nprod = (P.debug & 4096) ? 1 : NPROD;   // 4096: single producer (A/B)
+    if (prod >= 0) {
+        if (lane == 0) {
+            // ---------------- TMA producers (both CTAs; bytes land on the leader's barriers)
+            const uint32_t full0 = tc::mapa(tc::smem_u32(full), 0);
+            int stage = 0, it = 0;
+            uint32_t phase = 0;
+            for (int unit = pair; unit < units; unit += npairs) {
+                const int nt = unit / P.mtiles, mt = unit % P.mtiles;
+                const int tok = nt * SP_TILE_N + 96 * (int)rank;
+                const int rt = 2 * mt + (int)rank;
+                for (int kc = 0; kc < P.kchunks; ++kc, ++it) {
+                    if (it % nprod != prod) {
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
+                    tc::mbar_spin(&empty[stage], phase ^ 1);
+                    uint8_t *slot = ring + stage * SP_SLOT;
+                    const uint32_t fb = full0 + 8 * stage;
+                    if (rank == 0) tc::mbar_expect_tx(&full[stage], 2 * ((P.debug & 1024) ? SP_B : SP_SLOT));
+                    if (!(P.debug & 1024))
+                        tc::tma_load_2d_2sm(slot, &tmap_s, fb, 0, (rt * P.kchunks + kc) * (SP_IMG / 128));
+#ifdef SP_XEXP
+                    tc::tma_load_2d_2sm(slot + SP_IMG, &tmap_x, fb, tok, kc * BK);
+#else
+#pragma unroll
+                    for (int i = 0; i < 3; ++i)
+                        tc::tma_load_2d_2sm(slot + SP_IMG + i * SP_BATOM, &tmap_x, fb, tok + 32 * i, kc * BK);
+#endif
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            // ---------------- MMA issuer: leader CTA, one thread
+            const uint32_t idesc = tc::idesc_i8(256, SP_TILE_N, 0, 1) | (1u << 2);
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, acc_phase = 0, eslot = 0;
+            for (int unit = pair; unit < units; unit += npairs) {
+                tc::mbar_spin(&tempty[acc], acc_phase ^ 1);
+                tc::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * SP_TILE_N;
+                for (int kc = 0; kc < P.kchunks; ++kc) {
+                    tc::mbar_spin(&full[stage], phase);
+                    tc::tc_fence_after();
+                    const uint32_t a_addr = tc::smem_u32(ring + stage * SP_SLOT);
+                    const uint32_t e_tmem = tmem_base + SP_ECOL + 8 * eslot;
+                    tc::tmem_cp_128x128b_2sm(e_tmem, tc::smem_desc(a_addr + 8192, 2048, 128, 0));
+                    tc::tmem_cp_128x128b_2sm(e_tmem + 4, tc::smem_desc(a_addr + 10240, 2048, 128, 0));
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const uint64_t adesc = tc::smem_desc(a_addr + 256 * j, 128, 512, 0);
+                        const uint64_t bdesc = tc::smem_desc(a_addr + SP_IMG + 2048 * j, SP_BATOM, 256, 6);
+                        if (!(P.debug & 16))
+                            tc::mma_sp_i8_2sm(d_tmem, adesc, bdesc, e_tmem + 4 * j, idesc, (kc | j) ? 1u : 0u);
+                    }
+                    tc::mma_commit_2sm_mc(&empty[stage], 0x3);
+                    eslot ^= 1;
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                tc::mma_commit_2sm_mc(&tfull[acc], 0x3);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
+            }
+        }
+    } else if (warp < 2 + SP_EPI_WARPS) {
+        // ---------------- epilogue warps (both CTAs; each reads its own TMEM half)
+        const EpiWarp W = make_epi_warp<MODE, SP_EPI_WARPS>(warp, lane, staging, tables, E);
+        const uint32_t tempty0 = tc::mapa(tc::smem_u32(tempty), 0);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int unit = pair; unit < units; unit += npairs) {
+            const int nt = unit / P.mtiles, mt = unit % P.mtiles;
+            const uint32_t te = tempty0 + 8 * acc;
+            uint64_t *tf = &tfull[acc];
+            const uint32_t ph = acc_phase;
+            epi_tile<MODE, OUTK, true>(tmem_base, acc * SP_TILE_N, mt * 256 + 128 * (int)rank,
+                                       (int64_t)nt * SP_TILE_N, &tmap_o, P, E, W,
+                                       [tf, ph] { tc::mbar_wait(tf, ph); }, [te] { tc::mbar_arrive_cluster(te); });
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+        }
+        if ((OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA) && W.q == 2 && lane == 0) tc::tma_store_wait_all0();
+    }
+    tc::tc_fence_before();
+    tc::cluster_sync();
+    if (warp == 1) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc_2sm(tmem_base, 512);
+    }
+}
+
 // ---- host side ------------------------------------------------------------------
 int g_num_sms = 0;
 std::once_flag g_sms_once;
@@ -1009,7 +1426,7 @@ EncodeTiledFn encode_fn()
 }
 
 bool encode_2d(CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t outer, uint64_t pitch_bytes,
-               uint32_t box_inner, uint32_t box_outer)
+               uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B)
 {
     EncodeTiledFn enc = encode_fn();
     if (!enc) return false;
@@ -1018,7 +1435,7 @@ bool encode_2d(CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t outer, 
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(ptr), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -1029,7 +1446,31 @@ int env_int(const char *name, int dflt)
     return e ? atoi(e) : dflt;
 }
 
-enum Variant { V_SINGLE = 0, V_PAIR = 1, V_PAIR_XSTAT = 2, V_EXPAND = 3, V_EXPAND_XSTAT = 4 };
+enum Variant { V_SINGLE = 0, V_PAIR = 1, V_PAIR_XSTAT = 2, V_EXPAND = 3, V_EXPAND_XSTAT = 4, V_SPARSE = 5, V_MC2 = 6,
+               V_MC4 = 7 };
+
+// clusters of 2*XM CTAs that can be resident at once (persistent grid size)
+template <typename K>
+int max_clusters(K kern, int cluster, int threads, int smem, int fallback)
+{
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(cluster * 64, 1, 1);
+    cfg.blockDim = dim3(threads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, (void *)kern, &cfg) != cudaSuccess || n <= 0) {
+        cudaGetLastError();
+        return fallback;
+    }
+    return n;
+}
 
 int pick_mgroups(int mtiles, int ntiles, int npairs)
 {
@@ -1104,14 +1545,49 @@ int launch_mode(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx,
             return (int)cudaGetLastError();
         }
     }
-    if (variant == V_SINGLE) {
+    if (variant == V_MC2 || variant == V_MC4) {
+        const int XM = variant == V_MC2 ? 2 : 4;
+        const long units = (long)p.ntiles * (p.mtiles / XM);
+        if (XM == 2) {
+            auto kern = k2m_kernel<MODE, OUTK, 2>;
+            constexpr int smem = mc_smem<MODE, OUTK, 2>();
+            static_assert(smem <= SMEM_MAX, "shared memory budget");
+            static int ncl = 0;
+            if (!ncl) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                ncl = max_clusters(kern, 4, MT_THREADS, smem, sms / 4);
+            }
+            const int g = units < ncl ? (int)units : ncl;
+            kern<<<4 * g, MT_THREADS, smem, st>>>(tw, tx, to, p, E);
+        } else {
+            auto kern = k2m_kernel<MODE, OUTK, 4>;
+            constexpr int smem = mc_smem<MODE, OUTK, 4>();
+            static_assert(smem <= SMEM_MAX, "shared memory budget");
+            static int ncl = 0;
+            if (!ncl) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                ncl = max_clusters(kern, 8, MT_THREADS, smem, sms / 8);
+            }
+            const int g = units < ncl ? (int)units : ncl;
+            kern<<<8 * g, MT_THREADS, smem, st>>>(tw, tx, to, p, E);
+        }
+    } else if (variant == V_SPARSE) {
+        auto kern = k2s_kernel<MODE, OUTK>;
+        constexpr int smem = sp_smem<MODE, OUTK>();
+        static_assert(smem <= SMEM_MAX, "shared memory budget");
+        static bool attr = false;
+        if (!attr) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); attr = true; }
+        const int units = p.mtiles * p.ntiles;
+        const int pairs = units < sms / 2 ? units : sms / 2;
+        kern<<<2 * pairs, SP_THREADS, smem, st>>>(tw, tx, to, p, E);
+    } else if (variant == V_SINGLE) {
         auto kern = k2_tc_kernel<MODE, OUTK>;
         constexpr int smem = single_smem<MODE, OUTK>();
         static_assert(smem <= SMEM_MAX, "shared memory budget");
         static bool attr = false;
         if (!attr) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); attr = true; }
         const int tiles = p.mtiles * p.ntiles;
-        kern<<<tiles < sms ? tiles : sms, THREADS, smem, st>>>(tw, tx, to, p, E);
+        kern<<<tiles < sms ? tiles : sms, MT_THREADS, smem, st>>>(tw, tx, to, p, E);
     } else if (variant == V_PAIR) {
         auto kern = k2p_kernel<MODE, OUTK, false>;
         constexpr int smem = pair_smem<MODE, OUTK, false>();
@@ -1120,7 +1596,7 @@ int launch_mode(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx,
         if (!attr) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); attr = true; }
         const int units = p.mtiles * p.ntiles;
         const int pairs = units < sms / 2 ? units : sms / 2;
-        kern<<<2 * pairs, THREADS, smem, st>>>(tw, tx, to, p, E);
+        kern<<<2 * pairs, MT_THREADS, smem, st>>>(tw, tx, to, p, E);
     } else {
         auto kern = k2p_kernel<MODE, OUTK, true>;
         constexpr int smem = pair_smem<MODE, OUTK, true>();
@@ -1131,7 +1607,7 @@ int launch_mode(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx,
         p.mgroups = pick_mgroups(p.mtiles, p.ntiles, npairs);
         const long units = (long)p.ntiles * p.mgroups;
         const int pairs = units < npairs ? (int)units : npairs;
-        kern<<<2 * pairs, THREADS, smem, st>>>(tw, tx, to, p, E);
+        kern<<<2 * pairs, MT_THREADS, smem, st>>>(tw, tx, to, p, E);
     }
     return (int)cudaGetLastError();
 }
@@ -1174,31 +1650,52 @@ int k2_launch(const SpmmArgs &a)
         if (!e) return -1;
         std::string s(e);
         return s == "single" ? (int)V_SINGLE : s == "pair" ? (int)V_PAIR : s == "xstat" ? (int)V_PAIR_XSTAT
-             : s == "expand" ? (int)V_EXPAND : s == "expand_xstat" ? (int)V_EXPAND_XSTAT : -1;
+             : s == "expand" ? (int)V_EXPAND : s == "expand_xstat" ? (int)V_EXPAND_XSTAT
+             : s == "sparse" ? (int)V_SPARSE : s == "mc2" ? (int)V_MC2 : s == "mc4" ? (int)V_MC4 : -1;
     }();
     // the pair kernels tile W rows by 256; an odd count of 128-row tiles reads
     // one tile of TMA out-of-bounds zero fill
-    // measured defaults ("K2 variants"): single CTA for K <= 1024,
-    // CTA pair beyond; the X-stationary and expanded-W variants are kept
-    // selectable for the ongoing tuning
-    int variant = forced >= 0 ? forced : (h->tc_kpad <= KMAX_XSTAT ? V_SINGLE : V_PAIR);
+    // measured defaults ("K2 variants"): single CTA for small
+    // weights (K <= 1024 and M <= 1024), CTA pair otherwise; the other
+    // variants stay selectable (SI_K2_VARIANT) for tuning
+    int variant = forced >= 0 ? forced
+                              : ((h->tc_kpad <= KMAX_XSTAT && h->tc_mtiles <= 8) ? V_SINGLE : V_PAIR);
     if (variant == V_PAIR_XSTAT && h->tc_kpad > KMAX_XSTAT) variant = V_PAIR;
     if (variant == V_EXPAND_XSTAT && h->tc_kpad > KMAX_XSTAT) variant = V_EXPAND;
+    if (variant == V_SPARSE && a.layout != 0) variant = V_PAIR;   // k2s reads X as [K, N]
+    // X-sharing clusters: [K, N] activations and whole groups of XM pair tiles
+    if ((variant == V_MC2 || variant == V_MC4) && a.layout != 0) variant = V_PAIR;
+    if (variant == V_MC4 && ((h->tc_mtiles + 1) / 2) % 4) variant = V_MC2;
+    if (variant == V_MC2 && ((h->tc_mtiles + 1) / 2) % 2) variant = V_PAIR;
 
     CUtensorMap tw, tx, to;
-    const void *wt = img_sec<uint8_t>(a.img, h->off_tc_wt);
-    const uint64_t mpad = (uint64_t)h->tc_mtiles * 128;
-    if (!encode_2d(&tw, wt, mpad, (uint64_t)h->tc_kpad, mpad, 128, BK)) return (int)cudaErrorInvalidValue;
-    const uint32_t xbox_tok = variant == V_SINGLE ? TILE_N : 128;
     bool ok;
-    if (a.layout == 0)
-        ok = encode_2d(&tx, a.x, (uint64_t)a.n, (uint64_t)h->K, (uint64_t)a.ldx, 128, BK);
-    else
-        ok = encode_2d(&tx, a.x, (uint64_t)h->K, (uint64_t)a.n, (uint64_t)a.ldx, BK, xbox_tok);
+    if (variant == V_SPARSE) {
+        // the 2:4 images viewed as rows of 128 B, one 96-row box per (tile, chunk)
+        const uint64_t rows = (uint64_t)((h->tc_mtiles + 1) / 2 * 2) * (h->tc_kpad / BK) * (SP_IMG / 128);
+        ok = encode_2d(&tw, img_sec<uint8_t>(a.img, h->off_sp_img), 128, rows, 128, 128, SP_IMG / 128,
+                       CU_TENSOR_MAP_SWIZZLE_NONE) &&
+#ifdef SP_XEXP
+             encode_2d(&tx, a.x, (uint64_t)a.n, (uint64_t)h->K, (uint64_t)a.ldx, 128, BK);
+#else
+             encode_2d(&tx, a.x, (uint64_t)a.n, (uint64_t)h->K, (uint64_t)a.ldx, 32, BK, CU_TENSOR_MAP_SWIZZLE_32B);
+#endif
+    } else {
+        const void *wt = img_sec<uint8_t>(a.img, h->off_tc_wt);
+        const uint64_t mpad = (uint64_t)h->tc_mtiles * 128;
+        const uint32_t xbox_tok = variant == V_SINGLE ? TILE_N : 128;
+        const uint32_t xbox_k = variant == V_MC2 ? BK / 2 : variant == V_MC4 ? BK / 4 : BK;
+        ok = encode_2d(&tw, wt, mpad, (uint64_t)h->tc_kpad, mpad, 128, BK);
+        if (a.layout == 0)
+            ok = ok && encode_2d(&tx, a.x, (uint64_t)a.n, (uint64_t)h->K, (uint64_t)a.ldx, 128, xbox_k);
+        else
+            ok = ok && encode_2d(&tx, a.x, (uint64_t)h->K, (uint64_t)a.n, (uint64_t)a.ldx, BK, xbox_tok);
+    }
     if (!ok) return (int)cudaErrorInvalidValue;
     K2Params p;
+    const int tile_n = variant == V_SPARSE ? SP_TILE_N : TILE_N;
     p.mtiles = variant == V_SINGLE ? h->tc_mtiles : (h->tc_mtiles + 1) / 2;
-    p.ntiles = (int32_t)((a.n + TILE_N - 1) / TILE_N);
+    p.ntiles = (int32_t)((a.n + tile_n - 1) / tile_n);
     p.kchunks = h->tc_kpad / BK;
     p.b_mn_major = a.layout == 0 ? 1 : 0;
     p.mgroups = 1;
@@ -1208,6 +1705,10 @@ int k2_launch(const SpmmArgs &a)
     p.rqc = img_sec<float>(a.img, h->off_rqc);
     p.rqg = img_sec<float>(a.img, h->off_rqg);
     p.rtiles = h->tc_mtiles;
+    p.x = static_cast<const uint8_t *>(a.x);
+    p.ldx = a.ldx;
+    p.sp_rptr = img_sec<int32_t>(a.img, h->off_sp_rptr);
+    p.sp_res = img_sec<int32_t>(a.img, h->off_sp_res);
     p.debug = dbg;
     const bool out32 = h->out_dtype == 0 || h->out_dtype == 3;
     if (out32) {

@@ -107,6 +107,18 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo
     return d;
 }
 
+// general descriptor: layout 0 = SWIZZLE_NONE, 6 = SWIZZLE_32B, 2 = SWIZZLE_128B
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes, uint32_t layout)
+{
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)layout << 61;
+    return d;
+}
+
 // kind::i8 instruction descriptor: A = s8 (W), B = u8 (X), D = s32.
 __host__ __device__ constexpr uint32_t idesc_i8(uint32_t M, uint32_t N, uint32_t a_mn_major, uint32_t b_mn_major)
 {
@@ -224,6 +236,17 @@ __device__ __forceinline__ void tma_load_2d_2sm(void *dst, const CUtensorMap *m,
         ::"r"(smem_u32(dst)), "l"((uint64_t)m), "r"(c0), "r"(c1), "r"(leader_bar)
         : "memory");
 }
+// TMA load multicast to every CTA of cta_mask (same smem offset in each); the
+// complete_tx lands on the barrier at the same offset in each destination CTA
+__device__ __forceinline__ void tma_load_2d_mc(void *dst, const CUtensorMap *m, uint64_t *bar, int32_t c0, int32_t c1,
+                                               uint16_t cta_mask)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3}], [%4], %5;"
+        ::"r"(smem_u32(dst)), "l"((uint64_t)m), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(cta_mask)
+        : "memory");
+}
 __device__ __forceinline__ void tmem_alloc_2sm(uint32_t *slot_smem, uint32_t cols)
 {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot_smem)),
@@ -244,6 +267,23 @@ __device__ __forceinline__ void mma_i8_2sm(uint32_t d_tmem, uint64_t adesc, uint
         "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
         : "memory");
+}
+// 2:4 sparse A (s8) x dense B (u8), M256 x N x K64 over the CTA pair; the
+// metadata tile sits in TMEM at e_tmem (4-column aligned, selector 0)
+__device__ __forceinline__ void mma_sp_i8_2sm(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t e_tmem,
+                                              uint32_t idesc, uint32_t accum)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %5, 0;\n\t"
+        "tcgen05.mma.sp.cta_group::2.kind::i8 [%0], %1, %2, [%3], %4, p;\n}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(e_tmem), "r"(idesc), "r"(accum)
+        : "memory");
+}
+// smem [128 rows x 16 B] -> TMEM (128 lanes x 4 columns) in both CTAs of the pair
+__device__ __forceinline__ void tmem_cp_128x128b_2sm(uint32_t taddr, uint64_t sdesc)
+{
+    asm volatile("tcgen05.cp.cta_group::2.128x128b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
 }
 // arrive (once all prior MMAs of this thread complete) on the barrier at the
 // same offset in every CTA of cta_mask

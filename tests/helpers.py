@@ -40,3 +40,40 @@ def golden_case(d, meta, i):
 
 def has_gelu(prog) -> bool:
     return bool(np.isin(prog.ops, [3, 8]).any())
+
+
+# ctypes mirror of the plan image header (csrc/image.h SiImage); test-side
+# only, used to inspect plan sections
+import ctypes as _ct  # noqa: E402
+
+
+class SiImageHeader(_ct.Structure):
+    _fields_ = [("magic", _ct.c_uint32), ("version", _ct.c_uint32), ("M", _ct.c_int32), ("K", _ct.c_int32),
+                ("rows", _ct.c_int32), ("groups", _ct.c_int32), ("padded_blocks", _ct.c_int64),
+                ("nnz_blocks", _ct.c_int64), ("tiles", _ct.c_int64), ("out_dtype", _ct.c_int32),
+                ("a_zp", _ct.c_int32), ("n_ops", _ct.c_int32), ("n_luts", _ct.c_int32), ("n_chans", _ct.c_int32),
+                ("n_sides", _ct.c_int32), ("epi_mode", _ct.c_int32), ("exact", _ct.c_int32),
+                ("q_scale", _ct.c_float), ("q_inv", _ct.c_float), ("q_zp", _ct.c_int32), ("q_lo", _ct.c_int32),
+                ("q_hi", _ct.c_int32), ("n_bp", _ct.c_int32), ("tc_mtiles", _ct.c_int32), ("tc_kpad", _ct.c_int32),
+                ("pad0", _ct.c_int32), ("pad1", _ct.c_int32)] + \
+               [(f, _ct.c_uint64) for f in ("off_tile_ptr", "off_tile_w", "off_tile_idx", "off_adj", "off_scale_in",
+                                            "off_ops", "off_fparams", "off_finv", "off_iparams", "off_luts",
+                                            "off_chans", "off_clut", "off_bp_x", "off_bp_v", "off_tc_wt",
+                                            "total_bytes", "off_rqc")] + \
+               [("bp_key_lo", _ct.c_int32), ("bp_shift", _ct.c_int32), ("bp_nbucket", _ct.c_int32),
+                ("pad2", _ct.c_int32), ("off_bp_key", _ct.c_uint64), ("off_bp_bucket", _ct.c_uint64),
+                ("tc_emax", _ct.c_int32), ("tc_nlists", _ct.c_int32), ("off_tc_eptr", _ct.c_uint64),
+                ("off_tc_ent", _ct.c_uint64), ("off_rqg", _ct.c_uint64), ("off_sp_img", _ct.c_uint64),
+                ("off_sp_rptr", _ct.c_uint64), ("off_sp_res", _ct.c_uint64), ("sp_nres", _ct.c_int32),
+                ("sp_maxres", _ct.c_int32), ("reserved3", _ct.c_uint64), ("reserved4", _ct.c_uint64)]
+
+
+def image_header(img: np.ndarray) -> SiImageHeader:
+    assert _ct.sizeof(SiImageHeader) == 368
+    h = SiImageHeader.from_buffer_copy(img[:368].tobytes())
+    assert h.total_bytes == img.size
+    return h
+
+
+def image_section(img: np.ndarray, off: int, dtype, count: int) -> np.ndarray:
+    return img[off:off + np.dtype(dtype).itemsize * count].view(dtype)

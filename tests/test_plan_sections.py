@@ -1,0 +1,75 @@
+"""CPU checks of plan-image sections that the GPU kernels rely on:
+the requant exactness proof (plan.cpp requant_row_exact) and the 2:4
+images + residual lists of the sparse tensor-core kernel (K2s)."""
+
+import numpy as np
+import pytest
+
+import paper_2306_16601_b200 as P
+from paper_2306_16601_b200 import workloads as W
+from paper_2306_16601_b200.kernels.spmm import _build_image
+from helpers import image_header, image_section
+
+
+def _plan(m, k, ratio, seed, program):
+    w, _, bias, scales = W.baseline_inputs(m, k, 1, ratio, seed, with_x=False)
+    sw = P.encode_sparse(w, scales)
+    prog = W.program(program, scales)
+    img, _ = _build_image(sw, prog, bias)
+    return w, bias, prog, img
+
+
+@pytest.mark.parametrize("m,k,ratio,seed", [(1024, 1024, 0.9, 11), (512, 768, 0.8, 3)])
+def test_requant_proof_brute_force(m, k, ratio, seed):
+    w, bias, prog, img = _plan(m, k, ratio, seed, "requant_u8")
+    h = image_header(img)
+    rqg = image_section(img, h.off_rqg, np.float32, m)
+    rqc = image_section(img, h.off_rqc, np.float32, m)
+    adj = image_section(img, h.off_adj, np.int32, m)
+    proven = rqg >= 1
+    assert proven.mean() > 0.1, "some rows should be proven exact"
+    g = rqg[~proven]
+    assert ((g >= 0) & (g <= 0.25)).all(), "other rows carry the certificate guard"
+    s_in = np.asarray(prog.scale_in, np.float32)
+    fp = np.float32(prog.fparams[0])
+    zp, lo, hi = (int(v) for v in np.asarray(prog.iparams).reshape(-1)[:3])
+    rng = np.random.default_rng(0)
+    for r in rng.choice(np.flatnonzero(rqg >= 1), 6, replace=False):
+        A = 255 * int(np.abs(w[r].astype(np.int64)).sum()) + abs(int(adj[r]))
+        a = np.arange(-A, A + 1, dtype=np.int64)
+        dev = np.rint((a.astype(np.float32) * rqc[r]).astype(np.float64)) + zp
+        ref = np.rint(a.astype(np.float64) * np.float64(s_in[r]) / np.float64(fp)) + zp
+        np.testing.assert_array_equal(np.clip(dev, lo, hi), np.clip(ref, lo, hi), err_msg=f"row {r}")
+
+
+@pytest.mark.parametrize("m,k,ratio", [(1024, 1024, 0.9), (200, 300, 0.5), (384, 200, 0.8)])
+def test_sparse_images_reconstruct_weight(m, k, ratio):
+    w, _, _, img = _plan(m, k, ratio, 5, "s32")
+    h = image_header(img)
+    mt, kch = h.tc_mtiles, h.tc_kpad // 128
+    mt_pad = (mt + 1) // 2 * 2
+    sp = image_section(img, h.off_sp_img, np.uint8, mt_pad * kch * 12288).reshape(mt_pad, kch, 12288)
+    rptr = image_section(img, h.off_sp_rptr, np.int32, mt * 128 + 1)
+    res = image_section(img, h.off_sp_res, np.int32, h.sp_nres)
+    D = np.zeros((mt_pad * 128, kch * 128), np.int64)
+    row = np.arange(128)[:, None]
+    pb = np.arange(64)[None, :]
+    rr = np.arange(128)
+    for rt in range(mt_pad):
+        for kc in range(kch):
+            t = sp[rt, kc]
+            a = t[(row // 8) * 512 + (pb // 16) * 128 + (row % 8) * 16 + pb % 16].view(np.int8).astype(np.int64)
+            for mma in range(2):
+                e = t[8192 + mma * 2048 + (row // 8) * 128 + (row % 8) * 16 + np.arange(8)[None, :]]
+                for wm in range(16):
+                    nib = ((e[:, wm // 2] >> (4 * (wm % 2))) & 0xF).astype(np.int64)
+                    i0, i1 = nib & 3, nib >> 2
+                    assert (i0 < i1).all()
+                    wl = mma * 16 + wm
+                    np.add.at(D, (rt * 128 + rr, kc * 128 + wl * 4 + i0), a[:, 2 * wl])
+                    np.add.at(D, (rt * 128 + rr, kc * 128 + wl * 4 + i1), a[:, 2 * wl + 1])
+    for r in range(mt * 128):
+        for ent in res[rptr[r]:rptr[r + 1]]:
+            D[r, ent >> 8] += np.int8(ent & 0xFF)
+    np.testing.assert_array_equal(D[:m, :k], w.astype(np.int64))
+    assert not D[m:].any() and not D[:, k:].any()

@@ -1,0 +1,86 @@
+// tma_bw.cu -- experiment harness (not part of the product library): TMA
+// streaming throughput vs ring depth / box size.  Every CTA streams boxes of
+// [rows x 128 B] from a 2D u8 tensor through a ring of S slots; a consumer
+// thread waits for each slot and releases it at once.  Built by tools/tma_bw.py.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../paper_2306_16601_b200/csrc/tc_ptx.cuh"
+
+__global__ void tma_bw_kernel(const __grid_constant__ CUtensorMap tm, int S, int box_rows, int iters, int rows_total,
+                              int stride_ctas, int nprod, int ncols)
+{
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
+    const int slot_bytes = box_rows * 128;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * slot_bytes);
+    uint64_t *empty = full + S;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+        tc::mbar_fence_init();
+        tc::tma_prefetch_desc(&tm);
+    }
+    __syncthreads();
+    const int nboxes = rows_total / box_rows;
+    const int w = threadIdx.x >> 5;
+    if (w >= 2 && w < 2 + (nprod < 0 ? -nprod : nprod) && (threadIdx.x & 31) == 0) {
+        // producer p issues iterations i = p, p + nprod, ... (slot i % S)
+        for (int i = w - 2; i < iters; i += (nprod < 0 ? -nprod : nprod)) {
+            const int stage = i % S;
+            const uint32_t phase = (uint32_t)((i / S) & 1);
+            tc::mbar_spin(&empty[stage], phase ^ 1);
+            tc::mbar_expect_tx(&full[stage], slot_bytes);
+            const unsigned q = (unsigned)blockIdx.x * (unsigned)stride_ctas + (unsigned)i;
+            const int b = (int)(q & (unsigned)(nboxes - 1)), col = (int)((q >> 4) & (unsigned)(ncols - 1));
+            tc::tma_load_2d(smem + stage * slot_bytes, &tm, &full[stage], col * 128, b * box_rows);
+        }
+    } else if (threadIdx.x == 32) {
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int i = 0; i < iters; ++i) {
+            tc::mbar_wait(&full[stage], phase);
+            if (nprod < 0) tc::mma_commit(&empty[stage]);   // release through the tensor pipe
+            else tc::mbar_arrive(&empty[stage]);
+            if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+    }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// returns GB/s (bytes delivered to smem / time), or < 0 on error
+extern "C" double tma_bw(const void *buf, long rows_total, int S, int box_rows, int iters, int ctas, int stride_ctas,
+                         int reps, int nprod, long pitch)
+{
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess) return -1;
+    CUtensorMap tm;
+    cuuint64_t dims[2] = {(cuuint64_t)pitch, (cuuint64_t)rows_total};
+    cuuint64_t strides[1] = {(cuuint64_t)pitch};
+    const int ncols = (int)(pitch / 128);
+    cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    if (reinterpret_cast<EncodeTiledFn>(fn)(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(buf), dims,
+                                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return -2;
+    const int smem = S * box_rows * 128 + 1024 + 2048;
+    if (cudaFuncSetAttribute(tma_bw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return -3;
+    tma_bw_kernel<<<ctas, 64 + 32 * (nprod < 0 ? -nprod : nprod), smem>>>(tm, S, box_rows, iters, (int)rows_total, stride_ctas, nprod, ncols);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    for (int r = 0; r < reps; ++r) tma_bw_kernel<<<ctas, 64 + 32 * (nprod < 0 ? -nprod : nprod), smem>>>(tm, S, box_rows, iters, (int)rows_total, stride_ctas, nprod, ncols);
+    cudaEventRecord(b);
+    if (cudaEventSynchronize(b) != cudaSuccess) return -4;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    return (double)ctas * iters * box_rows * 128.0 * reps / (ms * 1e-3) / 1e9;
+}
