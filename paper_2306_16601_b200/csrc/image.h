@@ -85,7 +85,9 @@ struct SiImage {
     uint64_t off_sp_rptr;    // i32   [tc_mtiles * 128 + 1] residual entry offsets per padded row
     uint64_t off_sp_res;     // i32   [n_res]  (k << 8) | (uint8)w
     int32_t sp_nres, sp_maxres;  // residual entries, max per row
-    uint64_t reserved3, reserved4;
+    uint64_t off_rqp;        // f32   [M]               requant multiplier c' of rows proven exact (rqg == 1):
+                             //                         out = bits(fma(f32(a), c', 1.5*2^23 + zp)) - bits(1.5*2^23)
+    uint64_t reserved4;
 };
 
 static_assert(sizeof(SiImage) % 16 == 0, "image header must stay 16-byte aligned");

@@ -265,7 +265,7 @@ Compiled compile_program(const si_program *p)
 }
 
 struct Layout {
-    uint64_t off[24];
+    uint64_t off[25];
     uint64_t total;
 };
 
@@ -278,31 +278,31 @@ struct ExpandLists {
     int32_t emax = 0;
 };
 
-// True when the device's requant rounding, rint(RN32(f32(a) * c)) + zp
-// clamped to [lo, hi] with c = f32(s / fp), equals the reference's
+// True when the device's proven-row requant, n(a) = bits(fma(f32(a), c,
+// 1.5*2^23 + zp)) - bits(1.5*2^23) = rint(a*c + zp) (one rounding, exact while
+// |a*c + zp| < 2^22) saturated to [lo, hi], equals the reference's
 // rint((f64(a) * s) / fp) + zp clamped (epilogue.py:218-228) for every
-// integer |a| <= A.  Both rounded values are monotone in a, so they agree
-// everywhere iff every output step (k-1 -> k, lo-zp < k <= hi-zp) happens at
-// the same a; each step is located from the estimate (k - 1/2) / (s / fp)
-// by exact evaluation of both expressions.
-static bool requant_row_exact(int64_t A, float s_in, float fp, float c, int32_t zp, int32_t lo, int32_t hi)
+// integer |a| <= A.  Both are monotone in a, so they agree everywhere iff
+// every output step (k-1 -> k, lo < k <= hi) happens at the same a; each
+// step is located from its estimate by exact evaluation of both sides.
+static bool requant_fma_exact(int64_t A, float s_in, float fp, float c, int32_t zp, int32_t lo, int32_t hi)
 {
     const double q = (double)s_in / (double)fp;
-    if (!(c != 0.0f) || !std::isfinite(c) || !std::isfinite(q) || q == 0.0) return false;
-    if ((double)A * std::fabs((double)c) >= 2097152.0) return false;   // |r| < 2^21: magic rint exact
+    if (!(c != 0.0f) || !std::isfinite(c) || !std::isfinite(q) || q == 0.0 || (c > 0) != (q > 0)) return false;
+    if ((double)A * std::fabs((double)c) + std::fabs((double)zp) >= 2097152.0) return false;
+    const float mz = 12582912.0f + (float)zp;
     const int64_t sg = c > 0 ? 1 : -1;
-    auto Rr = [&](int64_t t) {
-        const float af = (float)(sg * t);
-        const float r = af * c;
-        return (int64_t)std::nearbyint((double)r);
+    auto Rd = [&](int64_t t) {
+        const float u = std::fmaf((float)(sg * t), c, mz);
+        return (int64_t)u - 12582912;
     };
     auto Ry = [&](int64_t t) {
         const double y = ((double)(sg * t) * (double)s_in) / (double)fp;
-        return (int64_t)std::nearbyint(y);
+        return (int64_t)std::nearbyint(y) + zp;
     };
     auto step = [&](auto R, int64_t k, int64_t &out) {
         // smallest t in [-A, A + 1] with R(t) >= k (A + 1: never)
-        double est = std::ceil(((double)k - 0.5) / std::fabs(q));
+        double est = std::ceil(((double)(k - zp) - 0.5) / std::fabs(q));
         est = std::min(std::max(est, (double)-A), (double)(A + 1));
         int64_t t = (int64_t)est;
         int steps = 0;
@@ -311,11 +311,27 @@ static bool requant_row_exact(int64_t A, float s_in, float fp, float c, int32_t 
         out = t;
         return true;
     };
-    for (int64_t k = (int64_t)lo - zp + 1; k <= (int64_t)hi - zp; ++k) {
+    for (int64_t k = (int64_t)lo + 1; k <= (int64_t)hi; ++k) {
         int64_t tr = 0, ty = 0;
-        if (!step(Rr, k, tr) || !step(Ry, k, ty) || tr != ty) return false;
+        if (!step(Rd, k, tr) || !step(Ry, k, ty) || tr != ty) return false;
     }
     return true;
+}
+
+// Search f32 multipliers near f32(s / fp) for one that makes the proven-row
+// requant exact for this row (requant_fma_exact); 0 if none within 32 ulps.
+static float requant_find_multiplier(int64_t A, float s_in, float fp, int32_t zp, int32_t lo, int32_t hi)
+{
+    const float c0 = (float)((double)s_in / (double)fp);
+    if (requant_fma_exact(A, s_in, fp, c0, zp, lo, hi)) return c0;
+    float up = c0, dn = c0;
+    for (int i = 0; i < 32; ++i) {
+        up = std::nextafter(up, INFINITY);
+        dn = std::nextafter(dn, -INFINITY);
+        if (requant_fma_exact(A, s_in, fp, up, zp, lo, hi)) return up;
+        if (requant_fma_exact(A, s_in, fp, dn, zp, lo, hi)) return dn;
+    }
+    return 0.0f;
 }
 
 // K2s 2:4 images (see image.h).  A window (group, 4 consecutive k) keeps
@@ -574,6 +590,7 @@ static Layout make_layout(const si_weight *w, const si_program *p, const Compile
     put(21, sp.img.size());
     put(22, 4 * sp.rptr.size());
     put(23, 4 * sp.res.size());
+    put(24, 4 * M);
     l.total = cur;
     return l;
 }
@@ -628,6 +645,7 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
     h->off_sp_img = l.off[21];
     h->off_sp_rptr = l.off[22];
     h->off_sp_res = l.off[23];
+    h->off_rqp = l.off[24];
     h->sp_nres = (int32_t)sp.res.size();
     h->sp_maxres = sp.maxres;
     std::memcpy(base + h->off_sp_img, sp.img.data(), sp.img.size());
@@ -672,12 +690,13 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
 
     // per-row bound on |acc + adj| (u8 activations <= 255): rows whose bound
     // stays below 2^22 never leave the magic-number range (rqg >= 0).  For
-    // requant, rows where the f32 rounding provably matches the reference's
-    // f64 rounding for every reachable accumulator get rqg = 1 (no
-    // certificate); the other rows get the certificate guard 2^-22 * max|r|
-    // as a per-row constant (0 <= rqg <= 1/4).
+    // requant, rows with a multiplier c' (rqp) under which the one-rounding
+    // fma form provably matches the reference's f64 rounding for every
+    // reachable accumulator get rqg = 1 (no certificate); the other rows get
+    // the certificate guard 2^-22 * max|r| as a per-row constant (0 <= rqg <= 1/4).
     {
         float *rqg = (float *)(base + h->off_rqg);
+        float *rqp = (float *)(base + h->off_rqp);
         for (int32_t g = 0; g < G; ++g) {
             int64_t sabs[4] = {0, 0, 0, 0};
             for (int64_t q = w->group_ptr[g]; q < w->group_ptr[g + 1]; ++q)
@@ -690,13 +709,19 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
                 if (m >= M) break;
                 const int64_t a = adj[m] < 0 ? -(int64_t)adj[m] : (int64_t)adj[m];
                 const int64_t bound = 255 * sabs[r] + a;
-                if (bound >= 4194304) {
+                if (c.mode == EPI_REQUANT && bound < 16777216) {
+                    // proven rows: 1 = accumulator converts by the magic number
+                    // (|a| < 2^22), 2 = by I2F (|a| < 2^24, exact)
+                    const float cp = requant_find_multiplier(bound, p->scale_in[m], c.q_scale, c.q_zp, c.q_lo, c.q_hi);
+                    rqp[m] = cp;
+                    if (cp != 0.0f) rqg[m] = bound < 4194304 ? 1.0f : 2.0f;
+                }
+                if (rqg[m] >= 1.0f) {
+                } else if (bound >= 4194304) {
                     rqg[m] = -1.0f;
                 } else if (c.mode == EPI_REQUANT) {
                     const float cm = (float)((double)p->scale_in[m] / (double)c.q_scale);
-                    if (requant_row_exact(bound, p->scale_in[m], c.q_scale, cm, c.q_zp, c.q_lo, c.q_hi)) {
-                        rqg[m] = 1.0f;
-                    } else {
+                    {
                         // certificate guard 2^-22 * max|r| (max|r| <= bound * |c|), rounded up
                         const double g = (double)bound * std::fabs((double)cm) * 2.384185791015625e-07 * (1.0 + 1.0 / 1024);
                         rqg[m] = (float)std::min(g * (1.0 + 1e-6) + 1e-30, 0.25);

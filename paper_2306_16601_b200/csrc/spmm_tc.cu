@@ -92,7 +92,8 @@ struct K2Params {
     void *out;
     int64_t ldo;
     const float *rqc;    // requant c[m] = f32(scale_in[m] / fp)
-    const float *rqg;    // per-row bound (image off_rqg): < 0 unsafe, else requant guard
+    const float *rqg;    // per-row class (image off_rqg): < 0 unsafe, >= 1 proven, else requant guard
+    const float *rqp;    // proven rows' requant multiplier (image off_rqp)
     int32_t rtiles;      // 128-row weight tiles with expansion lists (k2x)
     const uint8_t *x;    // K2s residual: activations [K][ldx] (KN layout)
     int64_t ldx;
@@ -178,23 +179,43 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, i
         }
     }
     int32_t v[32];
-    if constexpr (MODE == EPI_REQUANT) {
+    if (P.debug & 32768) {
+        // experiment: trivial math, same packing / staging / stores
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = (int32_t)(r[j] + (uint32_t)adj);
+    } else if constexpr (MODE == EPI_REQUANT) {
         const int32_t adjM = (int32_t)((uint32_t)adj + (uint32_t)MAGIC_I);
         const int32_t qoff = MAGIC_I - E.q_zp;
         float emax = 0.0f;
         uint32_t umax = 0;
         const unsigned long long M2 = tc::f2pack(MAGIC_F, MAGIC_F), C2 = tc::f2pack(cq, cq);
         if (gm >= 1.0f) {   // (warp-uniform: all rows proven)
-            // every row of this warp is proven at plan time (requant_row_exact):
-            // the f32 rounding equals the reference's for all reachable accumulators
+            // every row of this warp has a plan-time multiplier c' (rqp) under
+            // which rint(a * c' + zp) (one fma rounding onto the magic number
+            // 1.5*2^23 + zp) equals the reference's output for every reachable
+            // accumulator (plan.cpp requant_fma_exact): no certificate
+            const unsigned long long MZ2 = tc::f2pack(MAGIC_F + (float)E.q_zp, MAGIC_F + (float)E.q_zp);
+            if (gm >= 2.0f) {
+                // some row may exceed the magic range (|a| < 2^24): I2F conversion
 #pragma unroll
-            for (int j = 0; j < 32; j += 2) {
-                const int32_t b0 = (int32_t)(r[j] + (uint32_t)adjM);
-                const int32_t b1 = (int32_t)(r[j + 1] + (uint32_t)adjM);
-                const unsigned long long af = tc::sub_f32x2(tc::f2pack(__int_as_float(b0), __int_as_float(b1)), M2);
-                const unsigned long long uu = tc::add_f32x2(tc::mul_f32x2(af, C2), M2);
-                v[j] = __float_as_int(tc::f2lo(uu)) - qoff;
-                v[j + 1] = __float_as_int(tc::f2hi(uu)) - qoff;
+                for (int j = 0; j < 32; j += 2) {
+                    const float a0 = __int2float_rn((int32_t)(r[j] + (uint32_t)adj));
+                    const float a1 = __int2float_rn((int32_t)(r[j + 1] + (uint32_t)adj));
+                    const unsigned long long uu = tc::fma_f32x2(tc::f2pack(a0, a1), C2, MZ2);
+                    v[j] = __float_as_int(tc::f2lo(uu)) - MAGIC_I;
+                    v[j + 1] = __float_as_int(tc::f2hi(uu)) - MAGIC_I;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; j += 2) {
+                    const int32_t b0 = (int32_t)(r[j] + (uint32_t)adjM);
+                    const int32_t b1 = (int32_t)(r[j + 1] + (uint32_t)adjM);
+                    const unsigned long long af =
+                        tc::sub_f32x2(tc::f2pack(__int_as_float(b0), __int_as_float(b1)), M2);
+                    const unsigned long long uu = tc::fma_f32x2(af, C2, MZ2);
+                    v[j] = __float_as_int(tc::f2lo(uu)) - MAGIC_I;
+                    v[j + 1] = __float_as_int(tc::f2hi(uu)) - MAGIC_I;
+                }
             }
         } else if (fast) {
             // every row of this warp provably stays within the magic-number
@@ -360,14 +381,20 @@ __device__ __forceinline__ void epi_tile(uint32_t tmem_base, uint32_t tmem_col, 
     // per-row constants: issue the loads before blocking on the accumulator
     const int32_t adj = mok ? __ldg(E.adj + m) : 0;
     const float s_in = mok ? __ldg(E.scale_in + m) : 0.0f;
-    float cq = 0.0f;
-    if (MODE == EPI_REQUANT) cq = mok ? __ldg(P.rqc + m) : 0.0f;
+    float cq = 0.0f, cp = 0.0f;
+    if (MODE == EPI_REQUANT) {
+        cq = mok ? __ldg(P.rqc + m) : 0.0f;
+        cp = mok ? __ldg(P.rqp + m) : 0.0f;
+    }
     const float gr = mok ? __ldg(P.rqg + m) : 1.0f;
-    const bool fast = !(P.debug & 256) && __all_sync(0xffffffffu, gr >= 0.0f);
-    // gm: 1 when every row of the warp is proven exact (no certificate), else
-    // this row's certificate guard (proven rows: 0)
+    // gm: 1 (2: I2F conversion) when every row of the warp is proven exact
+    // (no certificate), else this row's certificate guard (proven rows: 0);
+    // fast: every row stays inside the magic-number range
     const bool proven = !(P.debug & 256) && __all_sync(0xffffffffu, gr >= 1.0f);
-    const float gm = proven ? 1.0f : (gr >= 1.0f ? 0.0f : fmaxf(gr, 0.0f));
+    const bool wide = __any_sync(0xffffffffu, gr >= 2.0f);
+    const bool fast = !(P.debug & 256) && !wide && __all_sync(0xffffffffu, gr >= 0.0f);
+    const float gm = proven ? (wide ? 2.0f : 1.0f) : (gr >= 1.0f ? 0.0f : fmaxf(gr, 0.0f));
+    if (proven) cq = cp;
     int32_t rp0 = 0, rp1 = 0;
     if constexpr (RES) {
         if (mok) { rp0 = __ldg(P.sp_rptr + m); rp1 = __ldg(P.sp_rptr + m + 1); }
@@ -379,7 +406,19 @@ __device__ __forceinline__ void epi_tile(uint32_t tmem_base, uint32_t tmem_col, 
         if (W.q == 2 && W.lane == 0) tc::tma_store_wait_read0();
         tc::named_bar_sync(1 + W.g, 128);
     }
-    if (!(P.debug & 1)) {
+    if (P.debug & 16384) {
+        // experiment: TMEM loads only (no math, no stores)
+        uint32_t acc = 0;
+#pragma unroll 1
+        for (int c = 0; c < COLS / 32; ++c) {
+            uint32_t r[32];
+            tc::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(W.q * 32) << 16) + tmem_col + W.g * COLS + c * 32, r);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc ^= r[j];
+        }
+        if (acc == 0x12345678u && m == -1) reinterpret_cast<uint32_t *>(P.out)[0] = acc;
+    } else if (!(P.debug & 1)) {
 #pragma unroll 1
         for (int c = 0; c < COLS / 32; ++c) {
             const int col = W.g * COLS + c * 32;
@@ -394,7 +433,7 @@ __device__ __forceinline__ void epi_tile(uint32_t tmem_base, uint32_t tmem_col, 
     if constexpr (STAGED) {
         tc::fence_proxy_async_smem();
         tc::named_bar_sync(1 + W.g, 128);
-        if (W.q == 2 && W.lane == 0) {
+        if (W.q == 2 && W.lane == 0 && !(P.debug & 8192)) {   // 8192: experiment, no output store
             tc::tma_store_2d(tmap_o, W.stg, row0, (int32_t)(tok0 + W.g * COLS));
             tc::tma_store_commit();
         }
@@ -1655,11 +1694,10 @@ int k2_launch(const SpmmArgs &a)
     }();
     // the pair kernels tile W rows by 256; an odd count of 128-row tiles reads
     // one tile of TMA out-of-bounds zero fill
-    // measured defaults ("K2 variants"): single CTA for small
-    // weights (K <= 1024 and M <= 1024), CTA pair otherwise; the other
-    // variants stay selectable (SI_K2_VARIANT) for tuning
-    int variant = forced >= 0 ? forced
-                              : ((h->tc_kpad <= KMAX_XSTAT && h->tc_mtiles <= 8) ? V_SINGLE : V_PAIR);
+    // measured default ("K2 variants"): the CTA pair unless the
+    // weight has a single 128-row tile; the other variants stay selectable
+    // (SI_K2_VARIANT) for tuning
+    int variant = forced >= 0 ? forced : (h->tc_mtiles <= 1 ? V_SINGLE : V_PAIR);
     if (variant == V_PAIR_XSTAT && h->tc_kpad > KMAX_XSTAT) variant = V_PAIR;
     if (variant == V_EXPAND_XSTAT && h->tc_kpad > KMAX_XSTAT) variant = V_EXPAND;
     if (variant == V_SPARSE && a.layout != 0) variant = V_PAIR;   // k2s reads X as [K, N]
@@ -1704,6 +1742,7 @@ int k2_launch(const SpmmArgs &a)
     p.ldo = a.ldo;
     p.rqc = img_sec<float>(a.img, h->off_rqc);
     p.rqg = img_sec<float>(a.img, h->off_rqg);
+    p.rqp = img_sec<float>(a.img, h->off_rqp);
     p.rtiles = h->tc_mtiles;
     p.x = static_cast<const uint8_t *>(a.x);
     p.ldx = a.ldx;

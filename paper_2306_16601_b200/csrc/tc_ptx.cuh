@@ -189,6 +189,14 @@ __device__ __forceinline__ unsigned long long mul_f32x2(unsigned long long a, un
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
     return d;
 }
+// a * b + c with a single rounding per lane
+__device__ __forceinline__ unsigned long long fma_f32x2(unsigned long long a, unsigned long long b,
+                                                        unsigned long long c)
+{
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
 }  // namespace tc
 
 namespace tc {
@@ -304,6 +312,10 @@ namespace tc {
 // negligible next to the 16 epilogue warps)
 __device__ __forceinline__ void mbar_spin(uint64_t *b, uint32_t parity)
 {
+#ifdef SI_SPIN_TRYWAIT
+    mbar_wait(b, parity);
+    return;
+#endif
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "SPIN_%=:\n\t"

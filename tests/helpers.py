@@ -65,7 +65,7 @@ class SiImageHeader(_ct.Structure):
                 ("tc_emax", _ct.c_int32), ("tc_nlists", _ct.c_int32), ("off_tc_eptr", _ct.c_uint64),
                 ("off_tc_ent", _ct.c_uint64), ("off_rqg", _ct.c_uint64), ("off_sp_img", _ct.c_uint64),
                 ("off_sp_rptr", _ct.c_uint64), ("off_sp_res", _ct.c_uint64), ("sp_nres", _ct.c_int32),
-                ("sp_maxres", _ct.c_int32), ("reserved3", _ct.c_uint64), ("reserved4", _ct.c_uint64)]
+                ("sp_maxres", _ct.c_int32), ("off_rqp", _ct.c_uint64), ("reserved4", _ct.c_uint64)]
 
 
 def image_header(img: np.ndarray) -> SiImageHeader:

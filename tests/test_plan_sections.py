@@ -19,27 +19,33 @@ def _plan(m, k, ratio, seed, program):
     return w, bias, prog, img
 
 
-@pytest.mark.parametrize("m,k,ratio,seed", [(1024, 1024, 0.9, 11), (512, 768, 0.8, 3)])
-def test_requant_proof_brute_force(m, k, ratio, seed):
+@pytest.mark.parametrize("m,k,ratio,seed,nrows", [(1024, 1024, 0.9, 11, 8), (512, 768, 0.8, 3, 8),
+                                                   (256, 4096, 0.9, 13, 2)])
+def test_requant_proof_brute_force(m, k, ratio, seed, nrows):
+    """Rows the plan marks proven (rqg == 1) use out = rint(a * c' + zp)
+    (one rounding, the device's fma form) with the plan's multiplier c' (rqp);
+    enumerate every reachable accumulator and compare with the reference."""
     w, bias, prog, img = _plan(m, k, ratio, seed, "requant_u8")
     h = image_header(img)
     rqg = image_section(img, h.off_rqg, np.float32, m)
-    rqc = image_section(img, h.off_rqc, np.float32, m)
+    rqp = image_section(img, h.off_rqp, np.float32, m)
     adj = image_section(img, h.off_adj, np.int32, m)
     proven = rqg >= 1
-    assert proven.mean() > 0.1, "some rows should be proven exact"
+    assert proven.mean() > 0.9, "the multiplier search should prove most rows"
     g = rqg[~proven]
     assert ((g >= 0) & (g <= 0.25)).all(), "other rows carry the certificate guard"
     s_in = np.asarray(prog.scale_in, np.float32)
-    fp = np.float32(prog.fparams[0])
+    fp = np.float32(np.asarray(prog.fparams).reshape(-1)[0])
     zp, lo, hi = (int(v) for v in np.asarray(prog.iparams).reshape(-1)[:3])
     rng = np.random.default_rng(0)
-    for r in rng.choice(np.flatnonzero(rqg >= 1), 6, replace=False):
+    for r in rng.choice(np.flatnonzero(proven), nrows, replace=False):
         A = 255 * int(np.abs(w[r].astype(np.int64)).sum()) + abs(int(adj[r]))
-        a = np.arange(-A, A + 1, dtype=np.int64)
-        dev = np.rint((a.astype(np.float32) * rqc[r]).astype(np.float64)) + zp
-        ref = np.rint(a.astype(np.float64) * np.float64(s_in[r]) / np.float64(fp)) + zp
-        np.testing.assert_array_equal(np.clip(dev, lo, hi), np.clip(ref, lo, hi), err_msg=f"row {r}")
+        assert A < 1 << 24 and (A < 1 << 22 or rqg[r] == 2)
+        for a0 in range(-A, A + 1, 1 << 22):
+            a = np.arange(a0, min(a0 + (1 << 22), A + 1), dtype=np.int64).astype(np.float64)
+            dev = np.rint(a * np.float64(rqp[r]) + zp)      # exact: |a| < 2^24, 24-bit c'
+            ref = np.rint(a * np.float64(s_in[r]) / np.float64(fp)) + zp
+            np.testing.assert_array_equal(np.clip(dev, lo, hi), np.clip(ref, lo, hi), err_msg=f"row {r}")
 
 
 @pytest.mark.parametrize("m,k,ratio", [(1024, 1024, 0.9), (200, 300, 0.5), (384, 200, 0.8)])
