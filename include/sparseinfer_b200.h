@@ -134,6 +134,35 @@ int32_t si_spmm(const void *host_image, const void *dev_image, const void *x, in
                 int64_t ldx, int64_t n, const float *sides, void *out, int64_t ldo,
                 void *workspace, uint64_t workspace_bytes, int32_t kernel, void *stream);
 
+/* Host-buffer run (the reference's spmm_exec takes host arrays,
+ * spmm.py:283-333): x_host [K, ldx] (SI_ACT_KN) or [N, ldx] (SI_ACT_NK) and
+ * out_host [N, ldo] in host memory (pinned for full overlap).  Token chunks
+ * of chunk_n are pipelined: H2D of chunk i+1 and D2H of chunk i-1 overlap the
+ * kernel on chunk i (launched on `stream`), double-buffered in `workspace`
+ * (device, si_spmm_host_workspace_size bytes).  Returns when out_host is
+ * complete.  Programs with side inputs: SI_EUNSUPPORTED (use si_spmm). */
+int32_t si_spmm_host_workspace_size(const void *host_image, int64_t chunk_n, int32_t x_layout, int32_t kernel,
+                                    uint64_t *bytes);
+int32_t si_spmm_host(const void *host_image, const void *dev_image, const void *x_host, int32_t x_layout,
+                     int64_t ldx, int64_t n, void *out_host, int64_t ldo, void *workspace,
+                     uint64_t workspace_bytes, int64_t chunk_n, int32_t kernel, void *stream);
+
+/* Several independent host-buffer SpMMs (e.g. Q/K/V projections) as one
+ * pipelined chunk sequence, so the copy-in of one job overlaps the copy-out
+ * of the previous one.  Same rules as si_spmm_host per job. */
+typedef struct {
+    const void *host_image, *dev_image;
+    const void *x_host;
+    int32_t x_layout;
+    int64_t ldx, n;
+    void *out_host;
+    int64_t ldo;
+} si_host_job;
+int32_t si_spmm_host_batch_workspace_size(const si_host_job *jobs, int32_t count, int64_t chunk_n,
+                                          uint64_t *bytes);
+int32_t si_spmm_host_batch(const si_host_job *jobs, int32_t count, void *workspace, uint64_t workspace_bytes,
+                           int64_t chunk_n, int32_t kernel, void *stream);
+
 /* Number of kernels si_spmm launches for these arguments (for launch
  * accounting in bench.py). */
 int32_t si_spmm_launch_count(const void *host_image, int64_t n, int32_t x_layout, int32_t kernel);

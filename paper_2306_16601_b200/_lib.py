@@ -37,6 +37,11 @@ class SiPlanInfo(ctypes.Structure):
                 ("image_bytes", _u64)]
 
 
+class SiHostJob(ctypes.Structure):
+    _fields_ = [("host_image", _vp), ("dev_image", _vp), ("x_host", _vp), ("x_layout", _i32), ("ldx", _i64),
+                ("n", _i64), ("out_host", _vp), ("ldo", _i64)]
+
+
 _lib = None
 
 
@@ -61,8 +66,14 @@ def lib():
     L.si_spmm_workspace_size.argtypes = [_vp, _i64, _i32, _i32, ctypes.POINTER(_u64)]
     L.si_spmm_launch_count.argtypes = [_vp, _i64, _i32, _i32]
     L.si_spmm.argtypes = [_vp, _vp, _vp, _i32, _i64, _i64, _vp, _vp, _i64, _vp, _u64, _i32, _vp]
+    L.si_spmm_host_workspace_size.argtypes = [_vp, _i64, _i32, _i32, ctypes.POINTER(_u64)]
+    L.si_spmm_host.argtypes = [_vp, _vp, _vp, _i32, _i64, _i64, _vp, _i64, _vp, _u64, _i64, _i32, _vp]
+    L.si_spmm_host_batch_workspace_size.argtypes = [ctypes.POINTER(SiHostJob), _i32, _i64, ctypes.POINTER(_u64)]
+    L.si_spmm_host_batch.argtypes = [ctypes.POINTER(SiHostJob), _i32, _vp, _u64, _i64, _i32, _vp]
     for f in ("si_plan_image_size", "si_plan_image_build", "si_plan_info_get",
-              "si_spmm_workspace_size", "si_spmm_launch_count", "si_spmm"):
+              "si_spmm_workspace_size", "si_spmm_launch_count", "si_spmm",
+              "si_spmm_host_workspace_size", "si_spmm_host",
+              "si_spmm_host_batch_workspace_size", "si_spmm_host_batch"):
         getattr(L, f).restype = _i32
     if L.si_abi_version() != 1:
         raise RuntimeError("libsparseinfer_b200 ABI version mismatch")

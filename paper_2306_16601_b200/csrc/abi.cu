@@ -6,6 +6,7 @@
 // the epilogue form and the shape picks K1 (gather, CUDA cores) or K2
 // (tcgen05 tensor-core tiles).  All launches are on the caller's stream.
 #include <cuda_runtime.h>
+#include <mutex>
 #include <string>
 
 #include "../../include/sparseinfer_b200.h"
@@ -103,4 +104,224 @@ extern "C" int32_t si_spmm(const void *host_image, const void *dev_image, const 
         return SI_ECUDA;
     }
     return SI_OK;
+}
+
+// ---- host-buffer entry points ----------------------------------------------------
+// The reference's spmm_exec takes host arrays; si_spmm_host is that boundary
+// for callers without device buffers.  Token chunks are pipelined: while the
+// kernel runs on chunk i (caller's stream), chunk i+1 is copied in on one
+// internal stream and chunk i-1 copied out on another, with double-buffered
+// device chunks in the caller's workspace.  si_spmm_host_batch runs several
+// independent SpMMs (e.g. the Q/K/V projections, or config 5's linear set)
+// as one chunk sequence, so the copy directions of consecutive jobs overlap.
+namespace {
+
+constexpr uint64_t WS_ALIGN = 256;
+uint64_t align_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+
+int out_elem_bytes(const SiImage *h) { return (h->out_dtype == 0 || h->out_dtype == 3) ? 4 : 1; }
+
+struct HostLayout {
+    int64_t chunk, ldx_dev, ldo_dev;
+    uint64_t x_bytes, o_bytes, k_bytes;
+};
+
+HostLayout host_layout(const SiImage *h, int64_t chunk_n, int32_t x_layout)
+{
+    HostLayout L;
+    L.chunk = (int64_t)align_up((uint64_t)chunk_n, 256);
+    L.ldx_dev = x_layout == SI_ACT_KN ? L.chunk : (int64_t)align_up((uint64_t)h->K, 16);
+    L.ldo_dev = (int64_t)align_up((uint64_t)h->M, 16);
+    L.x_bytes = align_up(x_layout == SI_ACT_KN ? (uint64_t)h->K * L.chunk : (uint64_t)L.chunk * L.ldx_dev, WS_ALIGN);
+    L.o_bytes = align_up((uint64_t)L.chunk * L.ldo_dev * out_elem_bytes(h), WS_ALIGN);
+    // a short last chunk may select K1: reserve what either kernel needs
+    const uint64_t k1 = k1_workspace(h, L.chunk, x_layout), k2 = k2_workspace(h, L.chunk, x_layout);
+    L.k_bytes = align_up(k1 > k2 ? k1 : k2, WS_ALIGN);
+    return L;
+}
+
+std::mutex g_stream_mu;
+cudaStream_t g_copy_streams[64][2];
+bool g_copy_init[64];
+
+bool copy_streams(cudaStream_t &in, cudaStream_t &out)
+{
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
+    std::lock_guard<std::mutex> lk(g_stream_mu);
+    if (!g_copy_init[dev]) {
+        if (cudaStreamCreateWithFlags(&g_copy_streams[dev][0], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&g_copy_streams[dev][1], cudaStreamNonBlocking) != cudaSuccess)
+            return false;
+        g_copy_init[dev] = true;
+    }
+    in = g_copy_streams[dev][0];
+    out = g_copy_streams[dev][1];
+    return true;
+}
+
+int32_t check_job(const si_host_job &j, const SiImage *&h)
+{
+    h = check_image(j.host_image);
+    if (!h) return SI_EINVAL;
+    if (!j.dev_image || !j.x_host || !j.out_host || j.n <= 0) {
+        si_set_error("null pointer or N <= 0");
+        return SI_EINVAL;
+    }
+    if (j.x_layout != SI_ACT_KN && j.x_layout != SI_ACT_NK) {
+        si_set_error("bad activation layout");
+        return SI_EINVAL;
+    }
+    if ((j.x_layout == SI_ACT_KN && j.ldx < j.n) || (j.x_layout == SI_ACT_NK && j.ldx < h->K) || j.ldo < h->M) {
+        si_set_error("leading dimension smaller than the row");
+        return SI_EINVAL;
+    }
+    if (h->n_sides > 0) {
+        si_set_error("host-buffer entry point does not take side inputs (use si_spmm)");
+        return SI_EUNSUPPORTED;
+    }
+    return SI_OK;
+}
+
+// workspace: [x 0][x 1][out 0][out 1][kernel], each the max over the jobs
+struct BatchLayout {
+    uint64_t x_bytes = 0, o_bytes = 0, k_bytes = 0, total = 0;
+};
+
+int32_t batch_layout(const si_host_job *jobs, int32_t count, int64_t chunk_n, BatchLayout &B)
+{
+    if (count <= 0 || !jobs || chunk_n <= 0) {
+        si_set_error("empty batch or chunk <= 0");
+        return SI_EINVAL;
+    }
+    for (int32_t i = 0; i < count; ++i) {
+        const SiImage *h = nullptr;
+        int32_t rc = check_job(jobs[i], h);
+        if (rc != SI_OK) return rc;
+        const HostLayout L = host_layout(h, chunk_n, jobs[i].x_layout);
+        B.x_bytes = L.x_bytes > B.x_bytes ? L.x_bytes : B.x_bytes;
+        B.o_bytes = L.o_bytes > B.o_bytes ? L.o_bytes : B.o_bytes;
+        B.k_bytes = L.k_bytes > B.k_bytes ? L.k_bytes : B.k_bytes;
+    }
+    B.total = 2 * B.x_bytes + 2 * B.o_bytes + B.k_bytes;
+    return SI_OK;
+}
+
+}  // namespace
+
+extern "C" int32_t si_spmm_host_batch_workspace_size(const si_host_job *jobs, int32_t count, int64_t chunk_n,
+                                                     uint64_t *bytes)
+{
+    BatchLayout B;
+    int32_t rc = batch_layout(jobs, count, chunk_n, B);
+    if (rc == SI_OK) *bytes = B.total;
+    return rc;
+}
+
+extern "C" int32_t si_spmm_host_batch(const si_host_job *jobs, int32_t count, void *workspace,
+                                      uint64_t workspace_bytes, int64_t chunk_n, int32_t kernel, void *stream)
+{
+    BatchLayout B;
+    int32_t rc = batch_layout(jobs, count, chunk_n, B);
+    if (rc != SI_OK) return rc;
+    if (workspace_bytes < B.total || !workspace) {
+        si_set_error("workspace too small: need " + std::to_string(B.total) + " bytes");
+        return SI_ENOSPACE;
+    }
+    cudaStream_t s_cmp = (cudaStream_t)stream, s_in, s_out;
+    if (!copy_streams(s_in, s_out)) {
+        si_set_error("cannot create copy streams");
+        return SI_ECUDA;
+    }
+    uint8_t *ws = (uint8_t *)workspace;
+    uint8_t *xbuf[2] = {ws, ws + B.x_bytes};
+    uint8_t *obuf[2] = {ws + 2 * B.x_bytes, ws + 2 * B.x_bytes + B.o_bytes};
+    void *kws = B.k_bytes ? ws + 2 * B.x_bytes + 2 * B.o_bytes : nullptr;
+
+    cudaEvent_t ev_entry, ev_done, in_done[2], cmp_done[2], out_done[2];
+    cudaEvent_t *all[] = {&ev_entry, &ev_done, &in_done[0], &in_done[1], &cmp_done[0], &cmp_done[1],
+                          &out_done[0], &out_done[1]};
+    for (cudaEvent_t *e : all) cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+    // the workspace may still be in use by work queued earlier on the caller's stream
+    cudaEventRecord(ev_entry, s_cmp);
+    cudaStreamWaitEvent(s_in, ev_entry, 0);
+    int64_t seq = 0;   // chunk sequence number across the batch (buffer = seq & 1)
+    for (int32_t jb = 0; jb < count && rc == SI_OK; ++jb) {
+        const si_host_job &J = jobs[jb];
+        const SiImage *h = (const SiImage *)J.host_image;
+        const HostLayout L = host_layout(h, chunk_n, J.x_layout);
+        const int eb = out_elem_bytes(h);
+        const uint8_t *xh = (const uint8_t *)J.x_host;
+        uint8_t *oh = (uint8_t *)J.out_host;
+        for (int64_t n0 = 0; n0 < J.n && rc == SI_OK; n0 += L.chunk, ++seq) {
+            const int b = (int)(seq & 1);
+            const int64_t nc = J.n - n0 < L.chunk ? J.n - n0 : L.chunk;
+            // copy in: buffer b is free once the kernel two chunks back finished
+            if (seq >= 2) cudaStreamWaitEvent(s_in, cmp_done[b], 0);
+            cudaError_t e;
+            if (J.x_layout == SI_ACT_KN)
+                e = cudaMemcpy2DAsync(xbuf[b], (size_t)L.ldx_dev, xh + n0, (size_t)J.ldx, (size_t)nc, (size_t)h->K,
+                                      cudaMemcpyHostToDevice, s_in);
+            else
+                e = cudaMemcpy2DAsync(xbuf[b], (size_t)L.ldx_dev, xh + n0 * J.ldx, (size_t)J.ldx, (size_t)h->K,
+                                      (size_t)nc, cudaMemcpyHostToDevice, s_in);
+            if (e != cudaSuccess) {
+                rc = SI_ECUDA;
+                si_set_error(std::string("H2D: ") + cudaGetErrorString(e));
+                break;
+            }
+            cudaEventRecord(in_done[b], s_in);
+            // compute: after its input arrived and the output buffer was drained
+            cudaStreamWaitEvent(s_cmp, in_done[b], 0);
+            if (seq >= 2) cudaStreamWaitEvent(s_cmp, out_done[b], 0);
+            rc = si_spmm(J.host_image, J.dev_image, xbuf[b], J.x_layout, L.ldx_dev, nc, nullptr, obuf[b], L.ldo_dev,
+                         kws, B.k_bytes, kernel, s_cmp);
+            if (rc != SI_OK) break;
+            cudaEventRecord(cmp_done[b], s_cmp);
+            // copy out
+            cudaStreamWaitEvent(s_out, cmp_done[b], 0);
+            e = cudaMemcpy2DAsync(oh + n0 * J.ldo * eb, (size_t)J.ldo * eb, obuf[b], (size_t)L.ldo_dev * eb,
+                                  (size_t)h->M * eb, (size_t)nc, cudaMemcpyDeviceToHost, s_out);
+            if (e != cudaSuccess) {
+                rc = SI_ECUDA;
+                si_set_error(std::string("D2H: ") + cudaGetErrorString(e));
+                break;
+            }
+            cudaEventRecord(out_done[b], s_out);
+        }
+    }
+    // host outputs are complete when this returns; later work on the caller's
+    // stream is ordered after the last copy
+    cudaEventRecord(ev_done, s_out);
+    cudaStreamWaitEvent(s_cmp, ev_done, 0);
+    cudaError_t e = cudaStreamSynchronize(s_out);
+    if (rc == SI_OK && e != cudaSuccess) {
+        rc = SI_ECUDA;
+        si_set_error(std::string("host pipeline: ") + cudaGetErrorString(e));
+    }
+    for (cudaEvent_t *ev : all) cudaEventDestroy(*ev);
+    return rc;
+}
+
+extern "C" int32_t si_spmm_host_workspace_size(const void *host_image, int64_t chunk_n, int32_t x_layout,
+                                               int32_t kernel, uint64_t *bytes)
+{
+    (void)kernel;
+    const SiImage *h = check_image(host_image);
+    if (!h) return SI_EINVAL;
+    if (chunk_n <= 0 || !bytes || (x_layout != SI_ACT_KN && x_layout != SI_ACT_NK)) {
+        si_set_error("bad chunk size, layout or output pointer");
+        return SI_EINVAL;
+    }
+    const HostLayout L = host_layout(h, chunk_n, x_layout);
+    *bytes = 2 * L.x_bytes + 2 * L.o_bytes + L.k_bytes;
+    return SI_OK;
+}
+
+extern "C" int32_t si_spmm_host(const void *host_image, const void *dev_image, const void *x_host, int32_t x_layout,
+                                int64_t ldx, int64_t n, void *out_host, int64_t ldo, void *workspace,
+                                uint64_t workspace_bytes, int64_t chunk_n, int32_t kernel, void *stream)
+{
+    const si_host_job j{host_image, dev_image, x_host, x_layout, ldx, n, out_host, ldo};
+    return si_spmm_host_batch(&j, 1, workspace, workspace_bytes, chunk_n, kernel, stream);
 }

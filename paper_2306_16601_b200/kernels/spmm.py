@@ -262,6 +262,73 @@ def spmm_exec(plan: SpmmPlan, act: ActivationLayout, pool=None, sides=None, out=
     return _run(plan, act.data, act.orient, act.n, act.ld, sides, out, kernel)
 
 
+_HOST_WS: dict = {}
+
+
+def _host_job(plan: SpmmPlan, x, layout: str, out):
+    sw = plan.weight
+    m = sw.logical_rows
+    prog = plan.program
+    if prog.n_sides:
+        raise ValueError("spmm_exec_host: programs with side inputs need spmm_exec")
+    xt = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+    if xt.is_cuda or xt.dtype != torch.uint8 or xt.ndim != 2:
+        raise ValueError("spmm_exec_host: x must be a host u8 matrix")
+    if layout == "kn":
+        k, n = xt.shape
+    elif layout == "nk":
+        n, k = xt.shape
+    else:
+        raise ValueError("layout must be 'kn' or 'nk'")
+    if k != sw.cols or n != plan.n:
+        raise ValueError("activation does not match the plan")
+    if xt.stride(1) != 1:
+        xt = xt.contiguous()
+    dt = _TORCH_DT[prog.out_dtype]
+    if out is None:
+        out = torch.empty((n, m), dtype=dt).pin_memory()
+    elif tuple(out.shape) != (n, m) or out.dtype != dt or out.is_cuda or (m > 1 and out.stride(1) != 1):
+        raise ValueError("bad output buffer")
+    job = _lib.SiHostJob(_lib.ptr(plan.image), plan.image_dev.data_ptr(), xt.data_ptr(), _lib.LAYOUTS[layout],
+                         _ld(xt), n, out.data_ptr(), _ld(out))
+    return job, xt, out
+
+
+def spmm_exec_host_batch(items, chunk: int = 8192, kernel: str = "auto") -> list:
+    """Several independent spmm_exec calls on host buffers as one pipelined
+    chunk sequence (si_spmm_host_batch): ``items`` is a list of
+    (plan, x, layout, out) with out None for a new pinned tensor.  The
+    copy-in of one job overlaps the copy-out of the previous one."""
+    L = _lib.lib()
+    if not items:
+        return []
+    built = [_host_job(p, x, lay, o) for (p, x, lay, o) in items]
+    jobs = (_lib.SiHostJob * len(built))(*[b[0] for b in built])
+    dev = items[0][0].image_dev.device
+    need = ctypes.c_uint64(0)
+    _lib.check(L.si_spmm_host_batch_workspace_size(jobs, len(built), chunk, ctypes.byref(need)), "spmm_exec_host")
+    key = (dev.index, int(need.value))
+    ws = _HOST_WS.get(key)
+    if ws is None:
+        _HOST_WS.clear()
+        ws = _HOST_WS[key] = torch.empty(int(need.value), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    rc = L.si_spmm_host_batch(jobs, len(built), ws.data_ptr(), need.value, chunk, _lib.KERNELS[kernel], stream)
+    _lib.check(rc, "spmm_exec_host")
+    return [b[2] for b in built]
+
+
+def spmm_exec_host(plan: SpmmPlan, x, layout: str = "kn", out=None, chunk: int = 8192,
+                   kernel: str = "auto") -> torch.Tensor:
+    """spmm_exec on host buffers (the reference's call takes host arrays,
+    spmm.py:283-333): ``x`` is the logical [K, N] (layout "kn") or token-major
+    [N, K] ("nk") u8 activation in host memory, the result [N, M] comes back
+    in host memory (``out`` or a new pinned tensor).  Token chunks are
+    pipelined by the library (si_spmm_host): copy-in, kernel and copy-out of
+    neighbouring chunks overlap.  Pinned inputs give full overlap."""
+    return spmm_exec_host_batch([(plan, x, layout, out)], chunk=chunk, kernel=kernel)[0]
+
+
 def spmm_ref(sw: Sparse4x1Weight, a, program: EpilogueProgram | None = None, bias=None,
              sides=None) -> torch.Tensor:
     """Naive device oracle (spmm.py:401-427): ``a`` is the logical [K, N] u8

@@ -197,3 +197,40 @@ def test_validation_errors():
     with pytest.raises(ValueError):
         K.spmm_exec(plan, K.relayout_activation(x), sides=np.zeros((1, 64, 16), np.float32),
                     out=torch.empty((64, 16), dtype=torch.int32, device="cuda"))
+
+
+@pytest.mark.parametrize("layout", ["kn", "nk"])
+@pytest.mark.parametrize("program,n,chunk", [("requant_u8", 20000, 4096), ("s32", 3000, 1024),
+                                             ("deq_f32", 5000, 8192), ("gelu_erf_u8", 2500, 512)])
+def test_host_entry_point(layout, program, n, chunk):
+    """si_spmm_host (spmm_exec_host): host buffers in and out, token chunks
+    pipelined through the copy streams; identical to the oracle."""
+    w, x, bias, scales = baseline_inputs(768, 1024, n, 0.85, 21)
+    sw = P.encode_sparse(w, scales)
+    prog = workloads.program(program, scales)
+    plan = K.plan_spmm(sw, n, program=prog, bias=bias)
+    xh = torch.from_numpy(np.ascontiguousarray(x if layout == "kn" else x.T)).pin_memory()
+    got = K.spmm_exec_host(plan, xh, layout=layout, chunk=chunk).numpy()
+    check_equal(got, oracle.spmm_exec(sw, x, prog, bias), prog, (layout, program, n, chunk))
+    # pageable numpy input, default chunk
+    got2 = K.spmm_exec_host(plan, np.ascontiguousarray(x if layout == "kn" else x.T), layout=layout).numpy()
+    assert np.array_equal(got2.view(np.uint8), got.view(np.uint8))
+
+
+def test_host_batch_entry_point():
+    """si_spmm_host_batch: independent SpMMs with different shapes, layouts
+    and output dtypes in one pipelined chunk sequence."""
+    items, want = [], []
+    for (m, k, n, prog_kind, layout, seed) in [(1024, 768, 9000, "requant_u8", "kn", 31),
+                                               (512, 2048, 3000, "s32", "nk", 32),
+                                               (768, 256, 1500, "deq_f32", "kn", 33)]:
+        w, x, bias, scales = baseline_inputs(m, k, n, 0.9, seed)
+        sw = P.encode_sparse(w, scales)
+        prog = workloads.program(prog_kind, scales)
+        plan = K.plan_spmm(sw, n, program=prog, bias=bias)
+        xh = torch.from_numpy(np.ascontiguousarray(x if layout == "kn" else x.T)).pin_memory()
+        items.append((plan, xh, layout, None))
+        want.append((oracle.spmm_exec(sw, x, prog, bias), prog))
+    outs = K.spmm_exec_host_batch(items, chunk=2048)
+    for i, (o, (ref, prog)) in enumerate(zip(outs, want)):
+        check_equal(o.numpy(), ref, prog, ("batch job", i))
