@@ -167,6 +167,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "gather", "tc"])
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-graphs", action="store_true", help="launch eagerly instead of replaying CUDA graphs")
     ap.add_argument("--e2e-chunk", type=int, default=32768, help="token chunk of the host pipeline")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -205,17 +206,33 @@ def main():
         _lib.lib().si_spmm_launch_count(_lib.ptr(L["plan"].image), n, 0, _lib.KERNELS[args.kernel])
         for L in layers)
 
+    graphs = []
+
     def step(evs=None):
         for i, L in enumerate(layers):
             if evs is not None:
                 evs[i][0].record(stream)
-            K.spmm_exec(L["plan"], L["act"], out=L["out"], kernel=args.kernel)
+            if graphs:
+                graphs[i].replay()
+            else:
+                K.spmm_exec(L["plan"], L["act"], out=L["out"], kernel=args.kernel)
             if evs is not None:
                 evs[i][1].record(stream)
 
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
+    if not args.no_graphs:
+        # one CUDA graph per linear (the same si_spmm launch, captured): replay
+        # keeps the host's Python/ctypes overhead out of the device timeline
+        for L in layers:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                K.spmm_exec(L["plan"], L["act"], out=L["out"], kernel=args.kernel)
+            graphs.append(g)
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
 
     # ---- timed region: K steps, barrier + sync on both sides, device events
     per_layer = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -297,7 +314,8 @@ def main():
                        "global_tokens": n * world, "linears": [c.name for c in cells], "sparsity": 0.9,
                        "epilogue": "bias+requant u8 (scale 2.0, zp 128)", "kernel": args.kernel,
                        "l2": "no flush: each step touches ~768 MB >> 126 MB L2",
-                       "parallelism": f"token-shard x{world} (no collective)"},
+                       "parallelism": f"token-shard x{world} (no collective)",
+                       "launch": "eager" if args.no_graphs else "CUDA graph per linear (replay)"},
             "gpu_launches": launches_per_step * args.steps,
             "per_linear": per_layer_info,
             "roofline": {"bound": "hbm", "kernel": dc.name, "achieved": round(achieved, 1),
