@@ -624,27 +624,30 @@ constexpr int P_A = 128 * BK;        // 16 KB
 constexpr int P_B = 128 * BK;        // 16 KB
 constexpr int KMAX_XSTAT = 1024;     // resident X: 128 tokens x K <= 128 KB per CTA
 
-template <int MODE, int OUTK, bool XSTAT>
+// BKS: k per pipeline stage (128, or 256 for the big-stage variant pair256)
+template <int MODE, int OUTK, bool XSTAT, int BKS = BK>
 constexpr int pair_stages()
 {
     constexpr int fixed = staged_bytes<OUTK>() + table_bytes<MODE>() + 2048 + (XSTAT ? KMAX_XSTAT * 128 : 0);
-    constexpr int per = XSTAT ? P_A : (P_A + P_B);
+    constexpr int per = XSTAT ? 128 * BKS : 2 * 128 * BKS;
     constexpr int s = (SMEM_MAX - fixed) / per;
     return s > 8 ? 8 : s;
 }
-template <int MODE, int OUTK, bool XSTAT>
+template <int MODE, int OUTK, bool XSTAT, int BKS = BK>
 constexpr int pair_smem()
 {
-    return pair_stages<MODE, OUTK, XSTAT>() * (XSTAT ? P_A : P_A + P_B) + (XSTAT ? KMAX_XSTAT * 128 : 0) +
-           staged_bytes<OUTK>() + table_bytes<MODE>() + 1024 + 512;
+    return pair_stages<MODE, OUTK, XSTAT, BKS>() * (XSTAT ? 128 * BKS : 2 * 128 * BKS) +
+           (XSTAT ? KMAX_XSTAT * 128 : 0) + staged_bytes<OUTK>() + table_bytes<MODE>() + 1024 + 512;
 }
 
-template <int MODE, int OUTK, bool XSTAT>
+template <int MODE, int OUTK, bool XSTAT, int BKS = BK>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MT_THREADS, 1)
 k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
            const __grid_constant__ CUtensorMap tmap_o, const K2Params P, const EpiParams E)
 {
-    constexpr int STAGES = pair_stages<MODE, OUTK, XSTAT>();
+    static_assert(!XSTAT || BKS == BK, "X-stationary uses 128-k stages");
+    constexpr int P_A = 128 * BKS, P_B = 128 * BKS;
+    constexpr int STAGES = pair_stages<MODE, OUTK, XSTAT, BKS>();
     constexpr int SLOT = XSTAT ? P_A : (P_A + P_B);
     constexpr int XBYTES = XSTAT ? KMAX_XSTAT * 128 : 0;
     constexpr int XCH = KMAX_XSTAT / BK;             // 8 resident X chunks
@@ -738,12 +741,14 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
                         uint8_t *a_s = ring + stage * SLOT;
                         const uint32_t fb = full0 + 8 * stage;
                         if (rank == 0) tc::mbar_expect_tx(&full[stage], 2 * SLOT);
-                        tc::tma_load_2d_2sm(a_s, &tmap_w, fb, mt * 256 + 128 * (int)rank, kc * BK);
+                        // (debug 2 / 4: every W / X load from tile 0 -- experiments)
+                        const int lmt = (P.debug & 2) ? 0 : mt, ltok = (P.debug & 4) ? 128 * (int)rank : tok;
+                        tc::tma_load_2d_2sm(a_s, &tmap_w, fb, lmt * 256 + 128 * (int)rank, kc * BKS);
                         if (!XSTAT) {
                             if (P.b_mn_major)
-                                tc::tma_load_2d_2sm(a_s + P_A, &tmap_x, fb, tok, kc * BK);
+                                tc::tma_load_2d_2sm(a_s + P_A, &tmap_x, fb, ltok, kc * BKS);
                             else
-                                tc::tma_load_2d_2sm(a_s + P_A, &tmap_x, fb, kc * BK, tok);
+                                tc::tma_load_2d_2sm(a_s + P_A, &tmap_x, fb, kc * BKS, ltok);
                         }
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
@@ -771,13 +776,19 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
                         const uint32_t a_addr = tc::smem_u32(ring + stage * SLOT);
                         const uint32_t b_addr = XSTAT ? tc::smem_u32(xbuf + kc * P_B) : a_addr + P_A;
 #pragma unroll
-                        for (int kk = 0; kk < ((P.debug & 16) ? 0 : BK / 32); ++kk) {
+                        for (int kk = 0; kk < ((P.debug & 16) ? 0 : BKS / 32); ++kk) {
                             const uint64_t adesc = tc::smem_desc_sw128(a_addr + kk * 4096, P_A, 1024);
                             const uint64_t bdesc = P.b_mn_major ? tc::smem_desc_sw128(b_addr + kk * 4096, P_B, 1024)
                                                                 : tc::smem_desc_sw128(b_addr + kk * 32, 16, 1024);
                             tc::mma_i8_2sm(d_tmem, adesc, bdesc, idesc, (kc | kk) ? 1u : 0u);
                         }
-                        tc::mma_commit_2sm_mc(&empty[stage], 0x3);
+                        if (P.debug & 65536) {
+                            // experiment (with debug 16): release by plain mbarrier arrives
+                            tc::mbar_arrive(&empty[stage]);
+                            tc::mbar_arrive_cluster(tc::mapa(tc::smem_u32(&empty[stage]), 1));
+                        } else {
+                            tc::mma_commit_2sm_mc(&empty[stage], 0x3);
+                        }
                         if (XSTAT && mt == m_hi - 1) tc::mma_commit_2sm_mc(&xempty[kc], 0x3);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
@@ -1486,7 +1497,7 @@ int env_int(const char *name, int dflt)
 }
 
 enum Variant { V_SINGLE = 0, V_PAIR = 1, V_PAIR_XSTAT = 2, V_EXPAND = 3, V_EXPAND_XSTAT = 4, V_SPARSE = 5, V_MC2 = 6,
-               V_MC4 = 7 };
+               V_MC4 = 7, V_PAIR256 = 8 };
 
 // clusters of 2*XM CTAs that can be resident at once (persistent grid size)
 template <typename K>
@@ -1627,6 +1638,15 @@ int launch_mode(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx,
         if (!attr) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); attr = true; }
         const int tiles = p.mtiles * p.ntiles;
         kern<<<tiles < sms ? tiles : sms, MT_THREADS, smem, st>>>(tw, tx, to, p, E);
+    } else if (variant == V_PAIR256) {
+        auto kern = k2p_kernel<MODE, OUTK, false, 256>;
+        constexpr int smem = pair_smem<MODE, OUTK, false, 256>();
+        static_assert(smem <= SMEM_MAX, "shared memory budget");
+        static bool attr = false;
+        if (!attr) { cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); attr = true; }
+        const int units = p.mtiles * p.ntiles;
+        const int pairs = units < sms / 2 ? units : sms / 2;
+        kern<<<2 * pairs, MT_THREADS, smem, st>>>(tw, tx, to, p, E);
     } else if (variant == V_PAIR) {
         auto kern = k2p_kernel<MODE, OUTK, false>;
         constexpr int smem = pair_smem<MODE, OUTK, false>();
@@ -1690,7 +1710,8 @@ int k2_launch(const SpmmArgs &a)
         std::string s(e);
         return s == "single" ? (int)V_SINGLE : s == "pair" ? (int)V_PAIR : s == "xstat" ? (int)V_PAIR_XSTAT
              : s == "expand" ? (int)V_EXPAND : s == "expand_xstat" ? (int)V_EXPAND_XSTAT
-             : s == "sparse" ? (int)V_SPARSE : s == "mc2" ? (int)V_MC2 : s == "mc4" ? (int)V_MC4 : -1;
+             : s == "sparse" ? (int)V_SPARSE : s == "mc2" ? (int)V_MC2 : s == "mc4" ? (int)V_MC4
+             : s == "pair256" ? (int)V_PAIR256 : -1;
     }();
     // the pair kernels tile W rows by 256; an odd count of 128-row tiles reads
     // one tile of TMA out-of-bounds zero fill
@@ -1701,6 +1722,7 @@ int k2_launch(const SpmmArgs &a)
     if (variant == V_PAIR_XSTAT && h->tc_kpad > KMAX_XSTAT) variant = V_PAIR;
     if (variant == V_EXPAND_XSTAT && h->tc_kpad > KMAX_XSTAT) variant = V_EXPAND;
     if (variant == V_SPARSE && a.layout != 0) variant = V_PAIR;   // k2s reads X as [K, N]
+    if (variant == V_PAIR256 && a.layout != 0) variant = V_PAIR;  // 256-k boxes: [K, N] activations
     // X-sharing clusters: [K, N] activations and whole groups of XM pair tiles
     if ((variant == V_MC2 || variant == V_MC4) && a.layout != 0) variant = V_PAIR;
     if (variant == V_MC4 && ((h->tc_mtiles + 1) / 2) % 4) variant = V_MC2;
@@ -1722,8 +1744,9 @@ int k2_launch(const SpmmArgs &a)
         const void *wt = img_sec<uint8_t>(a.img, h->off_tc_wt);
         const uint64_t mpad = (uint64_t)h->tc_mtiles * 128;
         const uint32_t xbox_tok = variant == V_SINGLE ? TILE_N : 128;
-        const uint32_t xbox_k = variant == V_MC2 ? BK / 2 : variant == V_MC4 ? BK / 4 : BK;
-        ok = encode_2d(&tw, wt, mpad, (uint64_t)h->tc_kpad, mpad, 128, BK);
+        const uint32_t bks = variant == V_PAIR256 ? 256 : BK;
+        const uint32_t xbox_k = variant == V_MC2 ? BK / 2 : variant == V_MC4 ? BK / 4 : bks;
+        ok = encode_2d(&tw, wt, mpad, (uint64_t)h->tc_kpad, mpad, 128, bks);
         if (a.layout == 0)
             ok = ok && encode_2d(&tx, a.x, (uint64_t)a.n, (uint64_t)h->K, (uint64_t)a.ldx, 128, xbox_k);
         else
@@ -1734,7 +1757,7 @@ int k2_launch(const SpmmArgs &a)
     const int tile_n = variant == V_SPARSE ? SP_TILE_N : TILE_N;
     p.mtiles = variant == V_SINGLE ? h->tc_mtiles : (h->tc_mtiles + 1) / 2;
     p.ntiles = (int32_t)((a.n + tile_n - 1) / tile_n);
-    p.kchunks = h->tc_kpad / BK;
+    p.kchunks = variant == V_PAIR256 ? (h->tc_kpad + 255) / 256 : h->tc_kpad / BK;
     p.b_mn_major = a.layout == 0 ? 1 : 0;
     p.mgroups = 1;
     p.N = a.n;

@@ -31,8 +31,17 @@ __global__ void tma_bw_kernel(const __grid_constant__ CUtensorMap tm, int S, int
             const uint32_t phase = (uint32_t)((i / S) & 1);
             tc::mbar_spin(&empty[stage], phase ^ 1);
             tc::mbar_expect_tx(&full[stage], slot_bytes);
-            const unsigned q = (unsigned)blockIdx.x * (unsigned)stride_ctas + (unsigned)i;
-            const int b = (int)(q & (unsigned)(nboxes - 1)), col = (int)((q >> 4) & (unsigned)(ncols - 1));
+            int b, col;
+            if (stride_ctas == 0) {
+                // disjoint: CTA c streams its own slice of the buffer
+                const int per = nboxes / (int)gridDim.x;
+                b = (int)blockIdx.x * per + (per ? i % per : 0);
+                col = 0;
+            } else {
+                const unsigned q = (unsigned)blockIdx.x * (unsigned)stride_ctas + (unsigned)i;
+                b = (int)(q & (unsigned)(nboxes - 1));
+                col = (int)((q >> 4) & (unsigned)(ncols - 1));
+            }
             tc::tma_load_2d(smem + stage * slot_bytes, &tm, &full[stage], col * 128, b * box_rows);
         }
     } else if (threadIdx.x == 32) {
@@ -83,4 +92,87 @@ extern "C" double tma_bw(const void *buf, long rows_total, int S, int box_rows, 
     float ms = 0;
     cudaEventElapsedTime(&ms, a, b);
     return (double)ctas * iters * box_rows * 128.0 * reps / (ms * 1e-3) / 1e9;
+}
+
+// ---- pair mode: cluster of 2, each CTA issues .cta_group::2 loads that
+// complete on the leader's barrier (as k2p does); the leader's consumer
+// releases the slot in both CTAs
+__global__ void __cluster_dims__(2, 1, 1) tma_bw2_kernel(const __grid_constant__ CUtensorMap tm, int S, int box_rows,
+                                                         int iters, int rows_total, int nprod, int boxes_per_stage)
+{
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
+    const int box_bytes = box_rows * 128;
+    const int slot_bytes = box_bytes * boxes_per_stage;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * slot_bytes);
+    uint64_t *empty = full + S;
+    const uint32_t rank = tc::cluster_ctarank();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+        tc::mbar_fence_init();
+        tc::tma_prefetch_desc(&tm);
+    }
+    tc::cluster_sync();
+    const int nboxes = rows_total / box_rows;
+    const int per = nboxes / (int)gridDim.x;
+    const int w = threadIdx.x >> 5;
+    const uint32_t full0 = tc::mapa(tc::smem_u32(full), 0);
+    if (w >= 2 && w < 2 + nprod && (threadIdx.x & 31) == 0) {
+        for (int i = w - 2; i < iters; i += nprod) {
+            const int stage = i % S;
+            const uint32_t phase = (uint32_t)((i / S) & 1);
+            tc::mbar_spin(&empty[stage], phase ^ 1);
+            if (rank == 0) tc::mbar_expect_tx(&full[stage], 2 * slot_bytes);
+            for (int j = 0; j < boxes_per_stage; ++j) {
+                const int b = (int)blockIdx.x * per + (per ? (i * boxes_per_stage + j) % per : 0);
+                tc::tma_load_2d_2sm(smem + stage * slot_bytes + j * box_bytes, &tm, full0 + 8 * stage, 0,
+                                    b * box_rows);
+            }
+        }
+    } else if (threadIdx.x == 32 && rank == 0) {
+        const uint32_t empty1 = tc::mapa(tc::smem_u32(empty), 1);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int i = 0; i < iters; ++i) {
+            tc::mbar_wait(&full[stage], phase);
+            tc::mbar_arrive(&empty[stage]);
+            tc::mbar_arrive_cluster(empty1 + 8 * stage);
+            if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+    }
+    tc::cluster_sync();
+}
+
+extern "C" double tma_bw2(const void *buf, long rows_total, int S, int box_rows, int iters, int ctas, int reps,
+                          int nprod, int boxes_per_stage)
+{
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess) return -1;
+    CUtensorMap tm;
+    cuuint64_t dims[2] = {128, (cuuint64_t)rows_total};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    if (reinterpret_cast<EncodeTiledFn>(fn)(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(buf), dims,
+                                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return -2;
+    const int smem = S * box_rows * 128 * boxes_per_stage + 1024 + 2048;
+    if (cudaFuncSetAttribute(tma_bw2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return -3;
+    tma_bw2_kernel<<<ctas, 64 + 32 * nprod, smem>>>(tm, S, box_rows, iters, (int)rows_total, nprod, boxes_per_stage);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    for (int r = 0; r < reps; ++r)
+        tma_bw2_kernel<<<ctas, 64 + 32 * nprod, smem>>>(tm, S, box_rows, iters, (int)rows_total, nprod,
+                                                        boxes_per_stage);
+    cudaEventRecord(b);
+    if (cudaEventSynchronize(b) != cudaSuccess) return -4;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    return (double)ctas * iters * box_rows * 128.0 * boxes_per_stage * reps / (ms * 1e-3) / 1e9;
 }

@@ -20,14 +20,16 @@ if __name__ == "__main__":
     L = ctypes.CDLL(SO)
     L.tma_bw.restype = ctypes.c_double
     L.tma_bw.argtypes = [ctypes.c_void_p, ctypes.c_long] + [ctypes.c_int] * 7 + [ctypes.c_long]
-    buf = torch.randint(0, 255, (64 << 20,), dtype=torch.uint8, device="cuda")
-    print("--- L2-resident 64 MB, 148 CTAs, box rows x 128 B, pitch 64 KB; producers < 0: tcgen05.commit release", flush=True)
-    pitch = 65536
-    rows = (64 << 20) // pitch
-    for box in (128, 256):
-        for S in (4, 8, 12):
-            if S * box * 128 > 200 * 1024:
-                continue
-            for nprod in (1, 2, 4, -1, -2):
-                bw = L.tma_bw(buf.data_ptr(), rows, S, box, 1024 * 128 // box, 148, 97, 5, nprod, pitch)
-                print(f"box {box} S {S:2d} producers {nprod:2d}: {bw:8.1f} GB/s", flush=True)
+    L.tma_bw2.restype = ctypes.c_double
+    L.tma_bw2.argtypes = [ctypes.c_void_p, ctypes.c_long] + [ctypes.c_int] * 7
+    buf = torch.randint(0, 255, (96 << 20,), dtype=torch.uint8, device="cuda")
+    rows = (96 << 20) // 128
+    print("--- disjoint 96 MB, 148 CTAs: 1-CTA loads vs pair (.cta_group::2) loads", flush=True)
+    for S in (6, 12):
+        for nprod in (1, 3):
+            bw = L.tma_bw(buf.data_ptr(), rows, S, 128, 1024, 148, 0, 5, nprod, 128)
+            print(f"1-CTA  S {S:2d} x 16 KB, producers {nprod}: {bw/148:6.1f} GB/s per SM", flush=True)
+    for (S, bps) in ((6, 2), (12, 1), (3, 4)):
+        for nprod in (1, 3):
+            bw = L.tma_bw2(buf.data_ptr(), rows, S, 128, 1024 // bps, 148, 5, nprod, bps)
+            print(f"pair   S {S:2d} x {bps} boxes of 16 KB, producers {nprod}: {bw/148:6.1f} GB/s per SM", flush=True)
