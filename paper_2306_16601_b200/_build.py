@@ -26,7 +26,7 @@ EXTRA_DEFS = os.environ.get("SI_BUILD_DEFS", "").split()
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off",
               "-Xptxas", "-v", "--expt-relaxed-constexpr"]
-SOURCES = ["plan.cpp", "abi.cu", "spmm_gather.cu", "spmm_tc.cu"]
+SOURCES = ["plan.cpp", "abi.cu", "spmm_gather.cu", "spmm_tc.cu", "spmm_tcx.cu"]
 
 
 def nvcc() -> str:
@@ -67,8 +67,20 @@ def build(force: bool = False, out: str | None = None) -> str:
     obj_dir = os.path.join(OUT_DIR, "obj" if out is None else "obj_exp")
     os.makedirs(obj_dir, exist_ok=True)
     objs = [os.path.join(obj_dir, s.rsplit(".", 1)[0] + ".o") for s in SOURCES]
-    with cf.ThreadPoolExecutor(len(SOURCES)) as ex:
-        list(ex.map(lambda so: _compile(so[0], so[1], obj_dir), zip(SOURCES, objs)))
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    headers.append(os.path.join(HERE, "..", "include", "sparseinfer_b200.h"))
+    newest_hdr = max(os.path.getmtime(h) for h in headers)
+
+    def needed(so):
+        src, obj = so
+        if force or not os.path.exists(obj):
+            return True
+        return os.path.getmtime(obj) < max(os.path.getmtime(os.path.join(CSRC, src)), newest_hdr)
+
+    todo = [so for so in zip(SOURCES, objs) if needed(so)]
+    if todo:
+        with cf.ThreadPoolExecutor(len(todo)) as ex:
+            list(ex.map(lambda so: _compile(so[0], so[1], obj_dir), todo))
     tmp = lib_path + ".tmp"
     cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -15,7 +15,8 @@
 #endif
 
 #define SI_IMG_MAGIC 0x58344953u /* "SI4X" */
-#define SI_IMG_VERSION 2u
+#define SI_IMG_VERSION 3u
+#define TR_SLOTS 128 /* K2t residual slots per 256-row pair tile */
 
 // compiled epilogue forms (see plan.cpp: compile_program)
 enum EpiMode : int32_t {
@@ -87,7 +88,14 @@ struct SiImage {
     int32_t sp_nres, sp_maxres;  // residual entries, max per row
     uint64_t off_rqp;        // f32   [M]               requant multiplier c' of rows proven exact (rqg == 1):
                              //                         out = bits(fma(f32(a), c', 1.5*2^23 + zp)) - bits(1.5*2^23)
-    uint64_t reserved4;
+    // K2t (X-stationary 2:4 kernel) residual operand, per 256-row pair tile
+    // pt: the columns that did not fit the main 2:4 images, gathered on-chip
+    // into TR_SLOTS slots of a second 2:4 operand (plan.cpp build_tr_sections)
+    uint64_t off_tr_img;     // bytes [2*pairs][12288]   residual 2:4 images (same format as sp_img)
+    uint64_t off_tr_k;       // u16   [pairs][TR_SLOTS]   activation column of each slot
+    uint64_t off_tr_cnt;     // i32   [pairs]             residual MMAs (64 slots each; 0..TR_SLOTS/64)
+    int32_t tr_ok, tr_pairs; // tr_ok 0: some pair tile needs more than TR_SLOTS slots (K2t unavailable)
+    uint64_t reserved5;
 };
 
 static_assert(sizeof(SiImage) % 16 == 0, "image header must stay 16-byte aligned");

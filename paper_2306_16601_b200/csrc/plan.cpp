@@ -9,6 +9,8 @@
 #include <cstdint>
 #include <cstring>
 #include <algorithm>
+#include <array>
+#include <map>
 #include <cfloat>
 #include <string>
 #include <vector>
@@ -265,7 +267,7 @@ Compiled compile_program(const si_program *p)
 }
 
 struct Layout {
-    uint64_t off[25];
+    uint64_t off[28];
     uint64_t total;
 };
 
@@ -342,7 +344,99 @@ struct SparseImages {
     std::vector<int32_t> rptr;
     std::vector<int32_t> res;
     int32_t maxres = 0;
+    // K2t residual operand (image.h): per 256-row pair tile
+    std::vector<uint8_t> tr_img;    // [pair tiles * 2][12288]
+    std::vector<uint16_t> tr_k;     // [pair tiles][TR_SLOTS]
+    std::vector<int32_t> tr_cnt;    // [pair tiles] residual MMAs (64 slots each)
+    int32_t tr_ok = 1;
 };
+
+// Write one 4-wide window of a 2:4 image tile (12 KB: compressed A
+// [128 rows x 64 B] K-major SWIZZLE_NONE core matrices + two metadata tiles):
+// window wl (0..31) of row `row`, entries (position in window, value) sorted by
+// position, at most two.
+static void sp_put_window(uint8_t *tile, int32_t row, int32_t wl, const std::pair<int32_t, uint8_t> *ent, int n)
+{
+    int32_t idx0 = 0, idx1 = 1;
+    uint8_t v0 = 0, v1 = 0;
+    if (n == 2) {
+        idx0 = ent[0].first; v0 = ent[0].second;
+        idx1 = ent[1].first; v1 = ent[1].second;
+    } else if (n == 1) {
+        if (ent[0].first == 3) { idx0 = 0; idx1 = 3; v1 = ent[0].second; }
+        else { idx0 = ent[0].first; idx1 = 3; v0 = ent[0].second; }
+    }
+    auto aoff = [&](int32_t pb) { return (row / 8) * 512 + (pb / 16) * 128 + (row % 8) * 16 + (pb % 16); };
+    tile[aoff(2 * wl)] = v0;
+    tile[aoff(2 * wl + 1)] = v1;
+    const int32_t mma = wl / 16, wm = wl % 16;
+    const uint8_t nib = (uint8_t)(idx0 | (idx1 << 2));
+    uint8_t *e = tile + 8192 + mma * 2048 + (row / 8) * 128 + (row % 8) * 16 + wm / 2;
+    *e = (uint8_t)((*e & ((wm % 2) ? 0x0F : 0xF0)) | ((wm % 2) ? (nib << 4) : nib));
+}
+
+// K2t: the residual columns of a 256-row pair tile become one more 2:4
+// operand over "slots": slot s holds activation column tr_k[s] (gathered
+// on-chip from the resident X tile), so the residual is one or two extra
+// sparse MMAs instead of per-element epilogue work.  Slots are assigned
+// greedily so that no row holds more than two entries in any 4-slot window;
+// a pair tile needing more than TR_SLOTS slots disables K2t (tr_ok = 0).
+static void build_tr_sections(SparseImages &S, const std::vector<std::vector<int32_t>> &rres, int32_t rt_n,
+                              int32_t rt_pad)
+{
+    const int32_t pt_n = rt_pad / 2;
+    S.tr_img.assign((size_t)rt_pad * 12288, 0);
+    S.tr_k.assign((size_t)pt_n * TR_SLOTS, 0);
+    S.tr_cnt.assign((size_t)pt_n, 0);
+    for (int32_t pt = 0; pt < pt_n; ++pt) {
+        // column -> rows (local 0..255) holding a residual there
+        std::map<int32_t, std::vector<std::pair<int32_t, uint8_t>>> bycol;
+        for (int32_t lr = 0; lr < 256; ++lr) {
+            const int32_t rt = 2 * pt + lr / 128;
+            if (rt >= rt_n) continue;
+            for (int32_t ent : rres[(size_t)rt * 128 + lr % 128]) bycol[ent >> 8].emplace_back(lr, (uint8_t)(ent & 0xFF));
+        }
+        std::vector<std::array<uint8_t, TR_SLOTS / 4>> cnt(256);
+        for (auto &c : cnt) c.fill(0);
+        std::vector<int32_t> slot_col(TR_SLOTS, -1);
+        std::vector<std::vector<std::pair<int32_t, uint8_t>>> slot_rows(TR_SLOTS);
+        int32_t used = 0;
+        for (auto &kv : bycol) {
+            int32_t s = 0;
+            for (; s < TR_SLOTS; ++s) {
+                if (slot_col[s] >= 0) continue;
+                bool ok = true;
+                for (auto &rv : kv.second)
+                    if (cnt[rv.first][s / 4] >= 2) { ok = false; break; }
+                if (ok) break;
+            }
+            if (s == TR_SLOTS) { S.tr_ok = 0; break; }
+            slot_col[s] = kv.first;
+            slot_rows[s] = kv.second;
+            for (auto &rv : kv.second) ++cnt[rv.first][s / 4];
+            used = std::max(used, s + 1);
+        }
+        if (!S.tr_ok) break;
+        S.tr_cnt[pt] = (used + 63) / 64;
+        for (int32_t s = 0; s < TR_SLOTS; ++s) S.tr_k[(size_t)pt * TR_SLOTS + s] = (uint16_t)std::max(slot_col[s], 0);
+        // per row and window: the (position, value) entries
+        std::vector<std::vector<std::pair<int32_t, uint8_t>>> win((size_t)256 * (TR_SLOTS / 4));
+        for (int32_t s = 0; s < TR_SLOTS; ++s)
+            for (auto &rv : slot_rows[s]) win[(size_t)rv.first * (TR_SLOTS / 4) + s / 4].emplace_back(s % 4, rv.second);
+        for (int32_t lr = 0; lr < 256; ++lr) {
+            uint8_t *tile = S.tr_img.data() + ((size_t)2 * pt + lr / 128) * 12288;
+            for (int32_t wl = 0; wl < TR_SLOTS / 4; ++wl) {
+                auto &e = win[(size_t)lr * (TR_SLOTS / 4) + wl];
+                std::sort(e.begin(), e.end());
+                sp_put_window(tile, lr % 128, wl, e.data(), (int)e.size());
+            }
+        }
+    }
+    if (!S.tr_ok) {
+        std::fill(S.tr_cnt.begin(), S.tr_cnt.end(), 0);
+        std::fill(S.tr_img.begin(), S.tr_img.end(), 0);
+    }
+}
 
 SparseImages build_sparse_images(const si_weight *w)
 {
@@ -437,6 +531,7 @@ SparseImages build_sparse_images(const si_weight *w)
         S.res.insert(S.res.end(), rres[r].begin(), rres[r].end());
     }
     S.rptr[rres.size()] = (int32_t)S.res.size();
+    build_tr_sections(S, rres, rt_n, rt_pad);
     return S;
 }
 
@@ -591,6 +686,9 @@ static Layout make_layout(const si_weight *w, const si_program *p, const Compile
     put(22, 4 * sp.rptr.size());
     put(23, 4 * sp.res.size());
     put(24, 4 * M);
+    put(25, sp.tr_img.size());
+    put(26, 2 * sp.tr_k.size());
+    put(27, 4 * sp.tr_cnt.size());
     l.total = cur;
     return l;
 }
@@ -648,6 +746,14 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
     h->off_rqp = l.off[24];
     h->sp_nres = (int32_t)sp.res.size();
     h->sp_maxres = sp.maxres;
+    h->off_tr_img = l.off[25];
+    h->off_tr_k = l.off[26];
+    h->off_tr_cnt = l.off[27];
+    h->tr_ok = sp.tr_ok;
+    h->tr_pairs = (int32_t)sp.tr_cnt.size();
+    std::memcpy(base + h->off_tr_img, sp.tr_img.data(), sp.tr_img.size());
+    std::memcpy(base + h->off_tr_k, sp.tr_k.data(), 2 * sp.tr_k.size());
+    std::memcpy(base + h->off_tr_cnt, sp.tr_cnt.data(), 4 * sp.tr_cnt.size());
     std::memcpy(base + h->off_sp_img, sp.img.data(), sp.img.size());
     std::memcpy(base + h->off_sp_rptr, sp.rptr.data(), 4 * sp.rptr.size());
     if (!sp.res.empty()) std::memcpy(base + h->off_sp_res, sp.res.data(), 4 * sp.res.size());

@@ -65,12 +65,14 @@ class SiImageHeader(_ct.Structure):
                 ("tc_emax", _ct.c_int32), ("tc_nlists", _ct.c_int32), ("off_tc_eptr", _ct.c_uint64),
                 ("off_tc_ent", _ct.c_uint64), ("off_rqg", _ct.c_uint64), ("off_sp_img", _ct.c_uint64),
                 ("off_sp_rptr", _ct.c_uint64), ("off_sp_res", _ct.c_uint64), ("sp_nres", _ct.c_int32),
-                ("sp_maxres", _ct.c_int32), ("off_rqp", _ct.c_uint64), ("reserved4", _ct.c_uint64)]
+                ("sp_maxres", _ct.c_int32), ("off_rqp", _ct.c_uint64), ("off_tr_img", _ct.c_uint64),
+                ("off_tr_k", _ct.c_uint64), ("off_tr_cnt", _ct.c_uint64), ("tr_ok", _ct.c_int32),
+                ("tr_pairs", _ct.c_int32), ("reserved5", _ct.c_uint64)]
 
 
 def image_header(img: np.ndarray) -> SiImageHeader:
-    assert _ct.sizeof(SiImageHeader) == 368
-    h = SiImageHeader.from_buffer_copy(img[:368].tobytes())
+    assert _ct.sizeof(SiImageHeader) == 400
+    h = SiImageHeader.from_buffer_copy(img[:400].tobytes())
     assert h.total_bytes == img.size
     return h
 

@@ -79,3 +79,51 @@ def test_sparse_images_reconstruct_weight(m, k, ratio):
             D[r, ent >> 8] += np.int8(ent & 0xFF)
     np.testing.assert_array_equal(D[:m, :k], w.astype(np.int64))
     assert not D[m:].any() and not D[:, k:].any()
+
+
+def _decode_sp_tile(t):
+    """(dense [128, 128] over the tile's 128 k / slot positions) of one 12 KB 2:4 image."""
+    row = np.arange(128)[:, None]
+    pb = np.arange(64)[None, :]
+    rr = np.arange(128)
+    a = t[(row // 8) * 512 + (pb // 16) * 128 + (row % 8) * 16 + pb % 16].view(np.int8).astype(np.int64)
+    D = np.zeros((128, 128), np.int64)
+    for mma in range(2):
+        e = t[8192 + mma * 2048 + (row // 8) * 128 + (row % 8) * 16 + np.arange(8)[None, :]]
+        for wm in range(16):
+            nib = ((e[:, wm // 2] >> (4 * (wm % 2))) & 0xF).astype(np.int64)
+            i0, i1 = nib & 3, nib >> 2
+            assert (i0 < i1).all()
+            wl = mma * 16 + wm
+            np.add.at(D, (rr, wl * 4 + i0), a[:, 2 * wl])
+            np.add.at(D, (rr, wl * 4 + i1), a[:, 2 * wl + 1])
+    return D
+
+
+@pytest.mark.parametrize("m,k,ratio", [(1024, 1024, 0.9), (520, 272, 0.8), (768, 768, 0.85), (4096, 1024, 0.9)])
+def test_k2t_residual_operand_reconstructs_weight(m, k, ratio):
+    """K2t: main 2:4 images + the per-pair-tile residual operand over slots
+    (slot s = activation column tr_k[s]) sum to W exactly; slots beyond the
+    tile's residual MMA count carry no weight."""
+    w, _, _, img = _plan(m, k, ratio, 7, "s32")
+    h = image_header(img)
+    assert h.tr_ok == 1
+    mt, kch = h.tc_mtiles, h.tc_kpad // 128
+    pt_n = (mt + 1) // 2
+    assert h.tr_pairs == pt_n
+    sp = image_section(img, h.off_sp_img, np.uint8, 2 * pt_n * kch * 12288).reshape(2 * pt_n, kch, 12288)
+    tri = image_section(img, h.off_tr_img, np.uint8, 2 * pt_n * 12288).reshape(2 * pt_n, 12288)
+    trk = image_section(img, h.off_tr_k, np.uint16, pt_n * 128).reshape(pt_n, 128).astype(np.int64)
+    cnt = image_section(img, h.off_tr_cnt, np.int32, pt_n)
+    assert ((cnt >= 0) & (cnt <= 2)).all()
+    D = np.zeros((2 * pt_n * 128, kch * 128), np.int64)
+    for rt in range(2 * pt_n):
+        for kc in range(kch):
+            D[rt * 128:(rt + 1) * 128, kc * 128:(kc + 1) * 128] += _decode_sp_tile(sp[rt, kc])
+        R = _decode_sp_tile(tri[rt])
+        used = 64 * cnt[rt // 2]
+        assert not R[:, used:].any()
+        for s in range(used):
+            D[rt * 128:(rt + 1) * 128, trk[rt // 2, s]] += R[:, s]
+    np.testing.assert_array_equal(D[:m, :k], w.astype(np.int64))
+    assert not D[m:].any() and not D[:, k:].any()

@@ -100,6 +100,8 @@ extern "C" double tma_bw(const void *buf, long rows_total, int S, int box_rows, 
 __global__ void __cluster_dims__(2, 1, 1) tma_bw2_kernel(const __grid_constant__ CUtensorMap tm, int S, int box_rows,
                                                          int iters, int rows_total, int nprod, int boxes_per_stage)
 {
+    const bool release_commit = nprod < 0;
+    if (nprod < 0) nprod = -nprod;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
     const int box_bytes = box_rows * 128;
@@ -135,8 +137,13 @@ __global__ void __cluster_dims__(2, 1, 1) tma_bw2_kernel(const __grid_constant__
         uint32_t phase = 0;
         for (int i = 0; i < iters; ++i) {
             tc::mbar_wait(&full[stage], phase);
-            tc::mbar_arrive(&empty[stage]);
-            tc::mbar_arrive_cluster(empty1 + 8 * stage);
+            if (release_commit) {
+                // release through the tensor pipe: 2-SM commit multicast to both CTAs
+                tc::mma_commit_2sm_mc(&empty[stage], 0x3);
+            } else {
+                tc::mbar_arrive(&empty[stage]);
+                tc::mbar_arrive_cluster(empty1 + 8 * stage);
+            }
             if (++stage == S) { stage = 0; phase ^= 1; }
         }
     }
@@ -162,14 +169,14 @@ extern "C" double tma_bw2(const void *buf, long rows_total, int S, int box_rows,
     const int smem = S * box_rows * 128 * boxes_per_stage + 1024 + 2048;
     if (cudaFuncSetAttribute(tma_bw2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
         return -3;
-    tma_bw2_kernel<<<ctas, 64 + 32 * nprod, smem>>>(tm, S, box_rows, iters, (int)rows_total, nprod, boxes_per_stage);
+    const int nthr = 64 + 32 * (nprod < 0 ? -nprod : nprod);
+    tma_bw2_kernel<<<ctas, nthr, smem>>>(tm, S, box_rows, iters, (int)rows_total, nprod, boxes_per_stage);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a);
     for (int r = 0; r < reps; ++r)
-        tma_bw2_kernel<<<ctas, 64 + 32 * nprod, smem>>>(tm, S, box_rows, iters, (int)rows_total, nprod,
-                                                        boxes_per_stage);
+        tma_bw2_kernel<<<ctas, nthr, smem>>>(tm, S, box_rows, iters, (int)rows_total, nprod, boxes_per_stage);
     cudaEventRecord(b);
     if (cudaEventSynchronize(b) != cudaSuccess) return -4;
     float ms = 0;
