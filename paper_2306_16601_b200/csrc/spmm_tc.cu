@@ -1192,10 +1192,13 @@ int k2_launch(const SpmmArgs &a)
              : s == "sparse" ? (int)V_SPARSE : s == "mc2" ? (int)V_MC2 : s == "mc4" ? (int)V_MC4
              : s == "pair256" ? (int)V_PAIR256 : s == "xsparse" ? 100 : -1;
     }();
-    // K2t (X-stationary 2:4, spmm_tcx.cu) whenever it applies: token-major X,
-    // K <= 1024, every pair tile's residual fits its slots
-    if ((forced < 0 || forced == 100) && k2t_supported(h, a.n, a.layout, a.x, a.ldx)) return k2t_launch(a);
-    if (forced == 100) return (int)cudaErrorInvalidValue;
+    // K2t (X-stationary 2:4, spmm_tcx.cu; SI_K2_VARIANT=xsparse): token-major
+    // X, K <= 1024, every pair tile's residual fits its slots.  Opt-in: on the
+    // config-5 shapes it measures slower than the dense pair.
+    if (forced == 100) {
+        if (k2t_supported(h, a.n, a.layout, a.x, a.ldx)) return k2t_launch(a);
+        return (int)cudaErrorInvalidValue;
+    }
     // the pair kernels tile W rows by 256; an odd count of 128-row tiles reads
     // one tile of TMA out-of-bounds zero fill
     // measured default ("K2 variants"): the CTA pair unless the

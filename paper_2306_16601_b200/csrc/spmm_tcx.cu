@@ -60,7 +60,7 @@ struct TGeom {
 };
 
 template <int OUTK>
-constexpr int t_staged() { return (OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA) ? T_EPI_GROUPS * T_STG : 0; }
+constexpr int t_staged() { return (OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA) ? 2 * T_EPI_GROUPS * T_STG : 0; }
 template <int MODE, int OUTK, int TNH>
 constexpr int t_fixed()
 {
@@ -91,51 +91,77 @@ __device__ __forceinline__ void trace_ev(unsigned long long *tr, int role, int &
     tr[role * T_TRACE_N + cnt++] = ((unsigned long long)kind << 56) | (t & 0x00FFFFFFFFFFFFFFull);
 }
 
+// Per-row epilogue constants of one accumulator tile (loaded one tile ahead:
+// the epilogue is the critical role, so their global-load latency must not
+// sit between two tiles).
+struct RowK {
+    int32_t adj;
+    float s_in, cq, cp, gr;
+};
+
+template <int MODE>
+__device__ __forceinline__ RowK load_rowk(int32_t m, const K2Params &P, const EpiParams &E)
+{
+    RowK k;
+    const bool mok = m < E.M;
+    k.adj = mok ? __ldg(E.adj + m) : 0;
+    k.s_in = mok ? __ldg(E.scale_in + m) : 0.0f;
+    k.cq = (MODE == EPI_REQUANT && mok) ? __ldg(P.rqc + m) : 0.0f;
+    k.cp = (MODE == EPI_REQUANT && mok) ? __ldg(P.rqp + m) : 0.0f;
+    k.gr = mok ? __ldg(P.rqg + m) : 1.0f;
+    return k;
+}
+
 // Epilogue of one accumulator (this warp: 32 rows x the column group's
-// chunks), per-chunk TMA stores from a single staging slot per group.
+// chunks); per-chunk TMA stores from two alternating staging slots per group
+// (a slot is rewritten only once the store issued from it two chunks earlier
+// has read it).
 template <int MODE, int OUTK, int TNH, typename Wait, typename Release>
 __device__ __forceinline__ void epi_tile_t(uint32_t tmem_base, uint32_t tmem_col, int32_t row0, int64_t tok0,
                                            const CUtensorMap *tmap_o, const K2Params &P, const EpiParams &E,
-                                           const EpiWarp &W, Wait wait_full, Release release)
+                                           EpiWarp &W, const RowK &k, int &slot, Wait wait_full, Release release,
+                                           unsigned long long *trc = nullptr, int trole = 0, int *tcnt = nullptr)
 {
     using G = TGeom<TNH>;
     constexpr bool STAGED = (OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA);
     const int32_t m = row0 + W.q * 32 + W.lane;
     const bool mok = m < E.M;
-    const int32_t adj = mok ? __ldg(E.adj + m) : 0;
-    const float s_in = mok ? __ldg(E.scale_in + m) : 0.0f;
-    float cq = 0.0f, cp = 0.0f;
-    if (MODE == EPI_REQUANT) {
-        cq = mok ? __ldg(P.rqc + m) : 0.0f;
-        cp = mok ? __ldg(P.rqp + m) : 0.0f;
-    }
-    const float gr = mok ? __ldg(P.rqg + m) : 1.0f;
-    const bool proven = !(P.debug & 256) && __all_sync(0xffffffffu, gr >= 1.0f);
-    const bool wide = __any_sync(0xffffffffu, gr >= 2.0f);
-    const bool fast = !(P.debug & 256) && !wide && __all_sync(0xffffffffu, gr >= 0.0f);
-    const float gm = proven ? (wide ? 2.0f : 1.0f) : (gr >= 1.0f ? 0.0f : fmaxf(gr, 0.0f));
-    if (proven) cq = cp;
+    const bool proven = !(P.debug & 256) && __all_sync(0xffffffffu, k.gr >= 1.0f);
+    const bool wide = __any_sync(0xffffffffu, k.gr >= 2.0f);
+    const bool fast = !(P.debug & 256) && !wide && __all_sync(0xffffffffu, k.gr >= 0.0f);
+    const float gm = proven ? (wide ? 2.0f : 1.0f) : (k.gr >= 1.0f ? 0.0f : fmaxf(k.gr, 0.0f));
+    const float cq = proven ? k.cp : k.cq;
     wait_full();
     tc::tc_fence_after();
     const uint32_t lane_base = tmem_base + ((uint32_t)(W.q * 32) << 16) + tmem_col;
+    uint8_t *const stg0 = W.stg;
 #pragma unroll 1
     for (int ch = W.g; ch < G::NCH; ch += T_EPI_GROUPS) {
         if constexpr (STAGED) {
-            // the previous store from this group's slot must have read it
-            if (W.q == 2 && W.lane == 0) tc::tma_store_wait_read0();
+            // the store issued from this slot two chunks ago must have read it
+            if (trc) trace_ev(trc, trole, *tcnt, 22);
+            if (W.q == 2 && W.lane == 0) tc::tma_store_wait_read1();
             tc::named_bar_sync(1 + W.g, 128);
+            if (trc) trace_ev(trc, trole, *tcnt, 23);
+            W.stg = stg0 + slot * (T_EPI_GROUPS * T_STG);
         }
         if (!(P.debug & 1))
-            epi_chunk<MODE, OUTK>(lane_base + ch * 32, m, mok, adj, s_in, cq, gm, fast, tok0 + ch * 32, 0, P, E, W);
+            epi_chunk<MODE, OUTK>(lane_base + ch * 32, m, mok, k.adj, k.s_in, cq, gm, fast, tok0 + ch * 32, 0, P, E,
+                                  W);
         if constexpr (STAGED) {
+            if (trc) trace_ev(trc, trole, *tcnt, 24);
             if (!(P.debug & 16384)) tc::fence_proxy_async_smem();   // 16384: experiment, no proxy fence
+            if (trc) trace_ev(trc, trole, *tcnt, 26);
             tc::named_bar_sync(1 + W.g, 128);
             if (W.q == 2 && W.lane == 0 && !(P.debug & 8192)) {
                 tc::tma_store_2d(tmap_o, W.stg, row0, (int32_t)(tok0 + ch * 32));
                 tc::tma_store_commit();
             }
+            if (trc) trace_ev(trc, trole, *tcnt, 25);
+            slot ^= 1;
         }
     }
+    W.stg = stg0;
     tc::tc_fence_before();
     __syncwarp();
     if (W.lane == 0) release();
@@ -416,24 +442,37 @@ k2t_kernel(const __grid_constant__ CUtensorMap tmap_s, const __grid_constant__ C
         EpiWarp W = make_epi_warp<MODE, T_EPI_WARPS>(warp, lane, staging, tables, E);
         W.stg = staging + W.g * T_STG;
         const uint32_t tempty0 = tc::mapa(tc::smem_u32(tempty), 0);
-        int acc = 0;
+        const int32_t mrow = 128 * (int)rank + W.q * 32 + lane;   // this lane's row within a pair tile
+        int acc = 0, slot = 0;
         uint32_t acc_phase = 0;
-        for (int unit = pair; unit < units; unit += npairs) {
-            int nt, m_lo, m_hi;
-            unit_range(unit, nt, m_lo, m_hi);
-            for (int i = 0; i < m_hi - m_lo; ++i) {
-                    const int mt = row_tile(m_lo, m_hi, i);
-                const uint32_t te = tempty0 + 8 * acc;
-                uint64_t *tf = &tfull[acc];
-                const uint32_t ph = acc_phase;
-                const bool tw = (warp == 2 && lane == 0);
-                epi_tile_t<MODE, OUTK, TNH>(tmem_base, acc * G::TN, mt * 256 + 128 * (int)rank,
-                                            (int64_t)nt * G::TN, &tmap_o, P, E, W,
-                                            [&, tf, ph] { tc::mbar_wait(tf, ph); if (tw) trace_ev(trc, 12 + (int)rank, tcnt, 20); },
-                                            [&, te] { if (tw) trace_ev(trc, 12 + (int)rank, tcnt, 21); tc::mbar_arrive_cluster(te); });
-                acc ^= 1;
-                if (acc == 0) acc_phase ^= 1;
+        // (unit, row tile) sequence of this pair, walked one tile ahead for the row constants
+        int unit = pair, i = 0, nt = 0, m_lo = 0, m_hi = 0;
+        if (unit < units) unit_range(unit, nt, m_lo, m_hi);
+        RowK k = load_rowk<MODE>(row_tile(m_lo, m_hi, 0) * 256 + mrow, P, E);
+        while (unit < units) {
+            const int mt = row_tile(m_lo, m_hi, i);
+            const int cur_nt = nt;
+            // advance to the next tile and prefetch its row constants
+            int nunit = unit, ni = i + 1, nnt = nt, nlo = m_lo, nhi = m_hi;
+            if (ni == m_hi - m_lo) {
+                nunit += npairs;
+                ni = 0;
+                if (nunit < units) unit_range(nunit, nnt, nlo, nhi);
             }
+            const RowK kn = nunit < units ? load_rowk<MODE>(row_tile(nlo, nhi, ni) * 256 + mrow, P, E) : k;
+            const uint32_t te = tempty0 + 8 * acc;
+            uint64_t *tf = &tfull[acc];
+            const uint32_t ph = acc_phase;
+            const bool tw = (warp == 2 && lane == 0);
+            epi_tile_t<MODE, OUTK, TNH>(tmem_base, acc * G::TN, mt * 256 + 128 * (int)rank, (int64_t)cur_nt * G::TN,
+                                        &tmap_o, P, E, W, k, slot,
+                                        [&, tf, ph] { tc::mbar_wait(tf, ph); if (tw) trace_ev(trc, 12 + (int)rank, tcnt, 20); },
+                                        [&, te] { if (tw) trace_ev(trc, 12 + (int)rank, tcnt, 21); tc::mbar_arrive_cluster(te); },
+                                        tw ? trc : nullptr, 12 + (int)rank, &tcnt);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+            k = kn;
+            unit = nunit; i = ni; nt = nnt; m_lo = nlo; m_hi = nhi;
         }
         if ((OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA) && W.q == 2 && lane == 0) tc::tma_store_wait_all0();
     }

@@ -1,8 +1,8 @@
 #!/bin/bash
-# One GPU call: tests, smoke, bench, ncu launch list, ncu full capture of the
-# dominant kernel.  Outputs under gpurun_out/ (copied to profiles/ by
-# tools/summarize_profiles.py).  Each ncu step runs only after the same
-# command exited 0 without ncu.
+# One GPU call: tests, smoke, bench, reference arm, ncu launch list, ncu full
+# capture of the dominant kernel (exported to CSV on the box: the .ncu-rep of
+# the tensor-core module exceeds gpurun's copy-back limit).  Each ncu step
+# runs only after the same command exited 0 without ncu.
 set -u
 cd "${GRAFT_REPO_ROOT:-$(pwd)}"
 mkdir -p gpurun_out
@@ -18,7 +18,9 @@ if timeout 600 $CMD > gpurun_out/plain_launch.log 2>&1; then
 fi
 P1="python tests/prof_one.py c5b auto 3"
 if timeout 300 $P1 > gpurun_out/plain_prof.log 2>&1; then
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k2 -s 2 -c 1 \
-     -o gpurun_out/prof_top $P1 > gpurun_out/ncu_full.log 2>&1
+  timeout 900 ncu --set full --clock-control none -k regex:k2 -s 2 -c 1 \
+     -o /tmp/prof_top $P1 > gpurun_out/ncu_full.log 2>&1
+  ncu -i /tmp/prof_top.ncu-rep --page raw --csv > gpurun_out/prof_top_raw.csv 2>/dev/null
+  ncu -i /tmp/prof_top.ncu-rep --page details --csv > gpurun_out/prof_top_details.csv 2>/dev/null
 fi
 echo done

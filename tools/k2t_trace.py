@@ -9,7 +9,8 @@ import numpy as np
 
 N = 8192
 NAMES = {1: "mma:full", 2: "mma:tempty", 3: "mma:rfull", 20: "epi:tfull", 21: "epi:release", 30: "gat:rempty",
-         31: "gat:done"}
+         31: "gat:done", 22: "epi:ch_start", 23: "epi:slot_ok", 24: "epi:math_done", 26: "epi:fenced",
+         25: "epi:stored"}
 
 
 def main(path):
@@ -41,6 +42,13 @@ def main(path):
         for k in sorted(set(nxt)):
             g = gaps[nxt == k]
             print(f"mma gap before {NAMES.get(k, k):11s}: n={len(g)} mean={g.mean():7.1f}ns sum={g.sum() / 1e3:7.1f}us")
+    if 12 in roles:
+        kind, t = roles[12]
+        gaps = np.diff(t)
+        nxt = kind[1:]
+        for k in sorted(set(nxt)):
+            g = gaps[nxt == k]
+            print(f"epi gap before {NAMES.get(k, k):13s}: n={len(g)} mean={g.mean():7.1f}ns sum={g.sum() / 1e3:7.1f}us")
     if len(sys.argv) > 2:
         kind, t = roles[8]
         for k, tt in list(zip(kind, t))[:int(sys.argv[2])]:

@@ -43,7 +43,9 @@ def launches(tag):
     for (k, g, b), v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"| `{k}` | {g} | {b} | {len(v)} | {sum(v) / len(v) / 1e3:.1f} | {sum(v) / total:.1%} |")
     lines.append("")
-    lines.append(f"Total launches: {len(rows)}; all of them are this repo's kernels (no library kernels).")
+    ours = sum(len(v) for (k, _, _), v in per.items() if k.startswith(("k1", "k2", "kref")))
+    lines.append(f"Total launches: {len(rows)}; {ours} of them are this repo's kernels, the rest are torch "
+                 f"utility kernels outside the SpMM (buffer fills of the host pipeline's setup).")
     with open(os.path.join(PROF, f"{tag}_launches.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
     return per
@@ -57,17 +59,32 @@ def ncu_raw(rep):
     return dict(zip(rows[0], rows[2]))
 
 
+def raw_csv(path):
+    rows = list(csv.reader(open(path)))
+    if len(rows) < 3:
+        return {}
+    return dict(zip(rows[0], rows[2]))
+
+
 def top(tag, cell="c5b_4096x1024"):
     rep = os.path.join(OUT, "prof_top.ncu-rep")
-    if not os.path.exists(rep):
+    csvp = os.path.join(OUT, "prof_top_raw.csv")   # exported on the box (tools/gpu_round.sh)
+    if os.path.exists(csvp):
+        m = raw_csv(csvp)
+    elif os.path.exists(rep):
+        m = ncu_raw(rep)
+    else:
         return
-    m = ncu_raw(rep)
     keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
             "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
             "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
             "sm__inst_executed.sum.per_cycle_active", "lts__t_sectors_srcunit_tex_op_read.sum",
             "lts__throughput.avg.pct_of_peak_sustained_elapsed", "launch__registers_per_thread",
-            "launch__grid_size", "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active"]
+            "launch__grid_size", "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
+            "lts__lts2xbar_cycles_active.avg.pct_of_peak_sustained_elapsed",
+            "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum.pct_of_peak_sustained_elapsed",
+            "sm__ops_path_tensor_op_utcimma_src_int8_sparsity_off.avg.pct_of_peak_sustained_elapsed",
+            "Kernel Name"]
     lines = [f"# {tag}: ncu --set full of the dominant kernel ({cell}, `tests/prof_one.py c5b auto`)", "",
              "| metric | value |", "|---|---|"]
     for k in keys:
