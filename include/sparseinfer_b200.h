@@ -167,6 +167,36 @@ int32_t si_spmm_host_batch(const si_host_job *jobs, int32_t count, void *workspa
  * accounting in bench.py). */
 int32_t si_spmm_launch_count(const void *host_image, int64_t n, int32_t x_layout, int32_t kernel);
 
+/* ---- dense f32 auxiliary operators (encoder composition, BASELINE config 4).
+ * Same fixed summation orders and expression trees as the reference's numba
+ * kernels, so results match element for element.  All pointers are device
+ * pointers; launches go to `stream`. */
+
+/* softmax over the last axis of a row-major [rows, n] tensor; replaces
+ * softmax_f32 (eltwise.py:34-59).  out may alias x. */
+int32_t si_softmax_rows_f32(const float *x, float *out, int64_t rows, int64_t n, void *stream);
+
+/* layer norm over the last axis of [rows, n] with affine gamma/beta [n];
+ * replaces layer_norm_f32 (eltwise.py:62-99). */
+int32_t si_layer_norm_f32(const float *x, const float *gamma, const float *beta, double eps, float *out,
+                          int64_t rows, int64_t n, void *stream);
+
+/* batched f32 matmul over a two-level batch (b0 < nb0, b1 < nb1): operand
+ * a at a + b0*sa0 + b1*sa1 is [m, k] with row stride lda; b likewise ([k, n],
+ * or [n, k] when transpose_b); out [m, n] with row stride ldo.  out = (a @ b)
+ * * alpha; replaces batch_matmul_f32 (eltwise.py:102-160) and covers the
+ * per-(sequence, head) attention products on token-major [N, H] tensors
+ * without copies. */
+int32_t si_bmm_f32(const float *a, const float *b, float *out, int64_t nb0, int64_t nb1, int64_t m, int64_t k,
+                   int64_t n, int64_t sa0, int64_t sa1, int64_t lda, int64_t sb0, int64_t sb1, int64_t ldb,
+                   int64_t so0, int64_t so1, int64_t ldo, int32_t transpose_b, float alpha, void *stream);
+
+/* per-tensor affine quantization of n floats: clamp(rint(f64 x / f64 scale) +
+ * zp, lo, hi) stored as u8 (lo >= 0) or s8 (lo < 0); replaces quantize
+ * (tensor.py:140-151) for per-tensor params. */
+int32_t si_quantize_f32(const float *x, int64_t n, float scale, int32_t zp, int32_t lo, int32_t hi, void *out,
+                        void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -61,6 +61,10 @@ def lib():
         L.orc_spmm_exec.argtypes = [i32, i32, i32, vp, vp, vp, vp, i64, i64, vp, vp,
                                     ctypes.POINTER(_Program), vp, vp, ctypes.c_int, ctypes.c_int]
         L.orc_gelu_array.argtypes = [vp, vp, i64, ctypes.c_int]
+        L.orc_softmax_rows.argtypes = [vp, vp, i64, i64]
+        L.orc_layer_norm_rows.argtypes = [vp, vp, vp, ctypes.c_double, vp, i64, i64]
+        L.orc_bmm.argtypes = [vp, vp, vp] + [i64] * 14 + [ctypes.c_int, ctypes.c_float]
+        L.orc_quantize.argtypes = [vp, i64, ctypes.c_float, i32, i32, i32, vp, ctypes.c_int]
         L.orc_max_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -185,3 +189,61 @@ def gelu(x: np.ndarray, erf: bool = False) -> np.ndarray:
 
 def max_threads() -> int:
     return int(lib().orc_max_threads())
+
+
+# ---- dense f32 auxiliary operators (eltwise.py), config-4 encoder composition ----
+
+def softmax_rows(x: np.ndarray) -> np.ndarray:
+    """softmax_f32 (eltwise.py:34-59) over the last axis."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.empty_like(x)
+    n = x.shape[-1]
+    lib().orc_softmax_rows(_p(x), _p(out), x.size // n, n)
+    return out
+
+
+def layer_norm(x: np.ndarray, gamma: np.ndarray, beta: np.ndarray, eps: float = 1e-5) -> np.ndarray:
+    """layer_norm_f32 (eltwise.py:62-99) over the last axis."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    gamma = np.ascontiguousarray(gamma, dtype=np.float32)
+    beta = np.ascontiguousarray(beta, dtype=np.float32)
+    out = np.empty_like(x)
+    n = x.shape[-1]
+    lib().orc_layer_norm_rows(_p(x), _p(gamma), _p(beta), float(eps), _p(out), x.size // n, n)
+    return out
+
+
+def batch_matmul(a: np.ndarray, b: np.ndarray, transpose_b: bool = False, alpha: float = 1.0) -> np.ndarray:
+    """batch_matmul_f32 (eltwise.py:102-160): a [B, M, K], b [B, K, N] or [B, N, K]."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    b = np.ascontiguousarray(b, dtype=np.float32)
+    bs, m, k = a.shape
+    n = b.shape[1] if transpose_b else b.shape[2]
+    out = np.empty((bs, m, n), np.float32)
+    lib().orc_bmm(_p(a), _p(b), _p(out), bs, 1, m, k, n, m * k, 0, k, b.shape[1] * b.shape[2], 0, b.shape[2],
+                  m * n, 0, n, 1 if transpose_b else 0, float(np.float32(alpha)))
+    return out
+
+
+def attention_context(q: np.ndarray, k: np.ndarray, v: np.ndarray, batch: int, seq: int, heads: int) -> np.ndarray:
+    """Scaled dot-product attention of token-major q/k/v [batch*seq, H] per
+    (sequence, head) with the reference's ops: bmm_nt * 1/sqrt(d), softmax,
+    bmm_nn.  Returns the context [batch*seq, H] (heads concatenated)."""
+    H = q.shape[1]
+    d = H // heads
+    qh = np.ascontiguousarray(q.reshape(batch, seq, heads, d).transpose(0, 2, 1, 3).reshape(-1, seq, d))
+    kh = np.ascontiguousarray(k.reshape(batch, seq, heads, d).transpose(0, 2, 1, 3).reshape(-1, seq, d))
+    vh = np.ascontiguousarray(v.reshape(batch, seq, heads, d).transpose(0, 2, 1, 3).reshape(-1, seq, d))
+    alpha = np.float32(1.0 / np.sqrt(np.float64(d)))
+    s = batch_matmul(qh, kh, transpose_b=True, alpha=alpha)
+    p = softmax_rows(s)
+    c = batch_matmul(p, vh)
+    return np.ascontiguousarray(c.reshape(batch, heads, seq, d).transpose(0, 2, 1, 3).reshape(batch * seq, H))
+
+
+def quantize(x: np.ndarray, scale, zp: int, lo: int = 0, hi: int = 255) -> np.ndarray:
+    """quantize (tensor.py:140-151), per tensor."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.empty(x.shape, np.int8 if lo < 0 else np.uint8)
+    lib().orc_quantize(_p(x), x.size, float(np.float32(scale)), int(zp), int(lo), int(hi), _p(out), 1 if lo < 0 else 0)
+    return out

@@ -317,3 +317,98 @@ int orc_max_threads(void)
     return 1;
 #endif
 }
+
+/* ---- dense f32 auxiliary operators of the encoder composition (BASELINE
+ * config 4), restating eltwise.py with its fixed summation orders and
+ * expression trees (no FMA: -ffp-contract=off). ------------------------- */
+
+/* softmax over rows of n (eltwise.py:34-50): max in f32, e = f32(exp(f64 x -
+ * f64 m)) with glibc exp, s = sequential f64 sum of e, out = e * f32(1/s) */
+void orc_softmax_rows(const float *x, float *out, int64_t rows, int64_t n)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < rows; ++r) {
+        const float *xr = x + r * n;
+        float *o = out + r * n;
+        float m = xr[0];
+        for (int64_t i = 1; i < n; ++i)
+            if (xr[i] > m) m = xr[i];
+        double s = 0.0;
+        for (int64_t i = 0; i < n; ++i) {
+            float e = (float)exp((double)xr[i] - (double)m);
+            o[i] = e;
+            s += (double)e;
+        }
+        float inv = (float)(1.0 / s);
+        for (int64_t i = 0; i < n; ++i) o[i] = o[i] * inv;
+    }
+}
+
+/* layer norm over rows of n (eltwise.py:62-76): f64 sequential mean and
+ * variance, inv = f32(1/sqrt(v/n + eps)), y = (x - f32(mean)) * inv in f32,
+ * out = y * gamma + beta in f32 */
+void orc_layer_norm_rows(const float *x, const float *gamma, const float *beta, double eps, float *out,
+                         int64_t rows, int64_t n)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < rows; ++r) {
+        const float *xr = x + r * n;
+        float *o = out + r * n;
+        double s = 0.0;
+        for (int64_t i = 0; i < n; ++i) s += (double)xr[i];
+        double mean = s / (double)n;
+        double v = 0.0;
+        for (int64_t i = 0; i < n; ++i) {
+            double d = (double)xr[i] - mean;
+            v += d * d;
+        }
+        float inv = (float)(1.0 / sqrt(v / (double)n + eps));
+        float mean32 = (float)mean;
+        for (int64_t i = 0; i < n; ++i) {
+            float y = (xr[i] - mean32) * inv;
+            o[i] = y * gamma[i] + beta[i];
+        }
+    }
+}
+
+/* batched f32 matmul (eltwise.py:102-127) on strided operands: batch index
+ * (b0, b1) addresses a at a + b0*sa0 + b1*sa1 (rows lda apart), likewise b
+ * and out.  NN: out[i][j] = (sum_p a[i][p] * b[p][j]) * alpha, accumulated
+ * p = 0..k-1 in f32 from 0 (the reference's row-update loop gives each
+ * out[i][j] the same sequence); NT: b is [n][k].  Each product and sum is
+ * one f32 rounding. */
+void orc_bmm(const float *a, const float *b, float *out, int64_t nb0, int64_t nb1, int64_t m, int64_t k, int64_t n,
+             int64_t sa0, int64_t sa1, int64_t lda, int64_t sb0, int64_t sb1, int64_t ldb, int64_t so0, int64_t so1,
+             int64_t ldo, int transpose_b, float alpha)
+{
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t b0 = 0; b0 < nb0; ++b0)
+        for (int64_t b1 = 0; b1 < nb1; ++b1) {
+            const float *A = a + b0 * sa0 + b1 * sa1;
+            const float *B = b + b0 * sb0 + b1 * sb1;
+            float *O = out + b0 * so0 + b1 * so1;
+            for (int64_t i = 0; i < m; ++i)
+                for (int64_t j = 0; j < n; ++j) {
+                    float s = 0.0f;
+                    for (int64_t p = 0; p < k; ++p) {
+                        float bv = transpose_b ? B[j * ldb + p] : B[p * ldb + j];
+                        float prod = A[i * lda + p] * bv;
+                        s = s + prod;
+                    }
+                    O[i * ldo + j] = s * alpha;
+                }
+        }
+}
+
+/* per-tensor affine quantization (tensor.py:140-151): clamp(rint(f64 x /
+ * f64 scale) + zp, lo, hi) */
+void orc_quantize(const float *x, int64_t n, float scale, int32_t zp, int32_t lo, int32_t hi, void *out,
+                  int out_s8)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        int32_t q = quant_scalar((double)x[i], (double)scale, zp, lo, hi);
+        if (out_s8) ((int8_t *)out)[i] = (int8_t)q;
+        else ((uint8_t *)out)[i] = (uint8_t)q;
+    }
+}
