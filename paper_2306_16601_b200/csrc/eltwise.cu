@@ -129,49 +129,147 @@ __global__ void k_layer_norm_rows(const float *x, const float *gamma, const floa
     }
 }
 
-// batch_matmul_f32 (eltwise.py:102-127) on strided operands: one thread per
-// output element, the k-sum in order p = 0..k-1 in f32 from 0 (each product
-// and each sum one rounding), then * alpha.  32x32 output tiles; A rows and
-// the B panel staged in shared memory k-chunk by k-chunk.
-constexpr int BT = 32, BK = 32;
-__global__ void k_bmm(const float *a, const float *b, float *out, int64_t nb1, int64_t m, int64_t k, int64_t n,
-                      int64_t sa0, int64_t sa1, int64_t lda, int64_t sb0, int64_t sb1, int64_t ldb, int64_t so0,
-                      int64_t so1, int64_t ldo, int transpose_b, float alpha)
+// Whole-row variants: the warp's 32 rows are loaded into shared memory once
+// (row stride n+1: lane r walks row r conflict-free), so the three sequential
+// passes read smem and the global traffic is one coalesced read and write.
+// One warp per block; dynamic smem 32*(n+1)*4 bytes.
+__device__ __forceinline__ void load_rows(const float *x, int64_t ld, int64_t rows, int64_t r0, int n, float *t)
 {
-    __shared__ float As[BT][BK + 1];
-    __shared__ float Bs[BK][BT + 1];
+    const int lane = threadIdx.x & 31;
+    for (int r = 0; r < ROWS; ++r) {
+        const int64_t row = r0 + r;
+#pragma unroll 4
+        for (int c = lane; c < n; c += 32) t[r * (n + 1) + c] = row < rows ? x[row * ld + c] : 0.0f;
+    }
+    __syncwarp();
+}
+__device__ __forceinline__ void store_rows(float *out, int64_t ld, int64_t rows, int64_t r0, int n, const float *t)
+{
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    for (int r = 0; r < ROWS; ++r) {
+        const int64_t row = r0 + r;
+        if (row >= rows) break;
+#pragma unroll 4
+        for (int c = lane; c < n; c += 32) out[row * ld + c] = t[r * (n + 1) + c];
+    }
+}
+
+__global__ void k_softmax_rows_smem(const float *x, float *out, int64_t rows, int n)
+{
+    extern __shared__ float t_sm[];
+    const int lane = threadIdx.x & 31;
+    const int64_t r0 = (int64_t)blockIdx.x * ROWS;
+    load_rows(x, n, rows, r0, n, t_sm);
+    float *t = t_sm + lane * (n + 1);
+    float m = t[0];
+    for (int c = 1; c < n; ++c)
+        if (t[c] > m) m = t[c];
+    double s = 0.0;
+    for (int c = 0; c < n; ++c) {
+        const float e = (float)exp((double)t[c] - (double)m);
+        t[c] = e;
+        s = __dadd_rn(s, (double)e);
+    }
+    const float inv = (float)(1.0 / s);
+    for (int c = 0; c < n; ++c) t[c] = __fmul_rn(t[c], inv);
+    store_rows(out, n, rows, r0, n, t_sm);
+}
+
+__global__ void k_layer_norm_rows_smem(const float *x, const float *gamma, const float *beta, double eps, float *out,
+                                       int64_t rows, int n)
+{
+    extern __shared__ float t_sm[];
+    const int lane = threadIdx.x & 31;
+    const int64_t r0 = (int64_t)blockIdx.x * ROWS;
+    load_rows(x, n, rows, r0, n, t_sm);
+    float *t = t_sm + lane * (n + 1);
+    double s = 0.0;
+    for (int c = 0; c < n; ++c) s = __dadd_rn(s, (double)t[c]);
+    const double mean = __ddiv_rn(s, (double)n);
+    double v = 0.0;
+    for (int c = 0; c < n; ++c) {
+        const double d = __dsub_rn((double)t[c], mean);
+        v = __dadd_rn(v, __dmul_rn(d, d));
+    }
+    const float inv = (float)__ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__ddiv_rn(v, (double)n), eps)));
+    const float mean32 = (float)mean;
+    for (int c = 0; c < n; ++c) {
+        const float y = __fmul_rn(__fsub_rn(t[c], mean32), inv);
+        t[c] = __fadd_rn(__fmul_rn(y, __ldg(gamma + c)), __ldg(beta + c));
+    }
+    store_rows(out, n, rows, r0, n, t_sm);
+}
+
+constexpr int SMEM_ROWS_MAX = 200 * 1024;
+inline bool rows_fit(int64_t n) { return n <= 4096 && (int64_t)ROWS * (n + 1) * 4 <= SMEM_ROWS_MAX; }
+
+// batch_matmul_f32 (eltwise.py:102-127) on strided operands.  Each output's
+// k-sum runs in order p = 0..k-1 in f32 from 0 (each product and each sum
+// one rounding), then * alpha -- exactly the reference's sequence.  64x64
+// output tiles, 256 threads with 4x4 register blocks; A and B panels staged
+// in shared memory 16 k at a time, coalesced along each operand's contiguous
+// dimension.
+constexpr int BT = 64, BK = 16;
+__global__ void __launch_bounds__(256) k_bmm(const float *a, const float *b, float *out, int64_t nb1, int64_t m,
+                                             int64_t k, int64_t n, int64_t sa0, int64_t sa1, int64_t lda, int64_t sb0,
+                                             int64_t sb1, int64_t ldb, int64_t so0, int64_t so1, int64_t ldo,
+                                             int transpose_b, float alpha)
+{
+    __shared__ float As[BK][BT + 4];   // [p][i]
+    __shared__ float Bs[BK][BT + 4];   // [p][j]
     const int64_t bz = blockIdx.z, b0 = bz / nb1, b1 = bz % nb1;
     const float *A = a + b0 * sa0 + b1 * sa1;
     const float *B = b + b0 * sb0 + b1 * sb1;
     float *O = out + b0 * so0 + b1 * so1;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8 threads, 4 rows each
+    const int t = threadIdx.x;
+    const int tx = t & 15, ty = t >> 4;             // 16 x 16 threads, rows ty*4.., cols tx*4..
     const int64_t i0 = (int64_t)blockIdx.y * BT, j0 = (int64_t)blockIdx.x * BT;
-    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    float acc[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = 0.0f;
     for (int64_t p0 = 0; p0 < k; p0 += BK) {
-        for (int r = ty; r < BT; r += 8) {
-            const int64_t i = i0 + r, p = p0 + tx;
-            As[r][tx] = (i < m && p < k) ? A[i * lda + p] : 0.0f;
+        // A [m][k] rows: lanes along p
+        for (int e = t; e < BT * BK; e += 256) {
+            const int r = e / BK, p = e % BK;
+            const int64_t i = i0 + r, pp = p0 + p;
+            As[p][r] = (i < m && pp < k) ? A[i * lda + pp] : 0.0f;
         }
-        for (int r = ty; r < BK; r += 8) {
-            const int64_t p = p0 + r, j = j0 + tx;
-            float v = 0.0f;
-            if (p < k && j < n) v = transpose_b ? B[j * ldb + p] : B[p * ldb + j];
-            Bs[r][tx] = v;
+        if (transpose_b) {   // B [n][k]: lanes along p
+            for (int e = t; e < BT * BK; e += 256) {
+                const int r = e / BK, p = e % BK;
+                const int64_t j = j0 + r, pp = p0 + p;
+                Bs[p][r] = (j < n && pp < k) ? B[j * ldb + pp] : 0.0f;
+            }
+        } else {             // B [k][n]: lanes along j
+            for (int e = t; e < BT * BK; e += 256) {
+                const int p = e / BT, r = e % BT;
+                const int64_t j = j0 + r, pp = p0 + p;
+                Bs[p][r] = (j < n && pp < k) ? B[pp * ldb + j] : 0.0f;
+            }
         }
         __syncthreads();
         const int pk = (int)imin64(BK, k - p0);
         for (int p = 0; p < pk; ++p) {
-            const float bv = Bs[p][tx];
+            const float4 av = *reinterpret_cast<const float4 *>(&As[p][ty * 4]);
+            const float4 bv = *reinterpret_cast<const float4 *>(&Bs[p][tx * 4]);
+            const float ar[4] = {av.x, av.y, av.z, av.w}, br[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
-            for (int q = 0; q < 4; ++q) acc[q] = __fadd_rn(acc[q], __fmul_rn(As[ty + 8 * q][p], bv));
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = __fadd_rn(acc[u][v], __fmul_rn(ar[u], br[v]));
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int64_t i = i0 + ty + 8 * q, j = j0 + tx;
-        if (i < m && j < n) O[i * ldo + j] = __fmul_rn(acc[q], alpha);
-    }
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int64_t i = i0 + ty * 4 + u, j = j0 + tx * 4 + v;
+            if (i < m && j < n) O[i * ldo + j] = __fmul_rn(acc[u][v], alpha);
+        }
 }
 
 // quantize (tensor.py:140-151): clamp(rint(f64 x / f64 scale) + zp, lo, hi)
@@ -197,7 +295,14 @@ extern "C" int32_t si_softmax_rows_f32(const float *x, float *out, int64_t rows,
         return SI_EINVAL;
     }
     if (rows == 0) return SI_OK;
-    k_softmax_rows<<<grid_rows(rows), 128, 0, (cudaStream_t)stream>>>(x, out, rows, n, n);
+    if (rows_fit(n)) {
+        const int smem = ROWS * (int)(n + 1) * 4;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(k_softmax_rows_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        k_softmax_rows_smem<<<(unsigned)((rows + ROWS - 1) / ROWS), 32, smem, (cudaStream_t)stream>>>(x, out, rows,
+                                                                                                       (int)n);
+    } else {
+        k_softmax_rows<<<grid_rows(rows), 128, 0, (cudaStream_t)stream>>>(x, out, rows, n, n);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { si_set_error(cudaGetErrorString(e)); return SI_ECUDA; }
     return SI_OK;
@@ -211,7 +316,15 @@ extern "C" int32_t si_layer_norm_f32(const float *x, const float *gamma, const f
         return SI_EINVAL;
     }
     if (rows == 0) return SI_OK;
-    k_layer_norm_rows<<<grid_rows(rows), 128, 0, (cudaStream_t)stream>>>(x, gamma, beta, eps, out, rows, n);
+    if (rows_fit(n)) {
+        const int smem = ROWS * (int)(n + 1) * 4;
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(k_layer_norm_rows_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        k_layer_norm_rows_smem<<<(unsigned)((rows + ROWS - 1) / ROWS), 32, smem, (cudaStream_t)stream>>>(
+            x, gamma, beta, eps, out, rows, (int)n);
+    } else {
+        k_layer_norm_rows<<<grid_rows(rows), 128, 0, (cudaStream_t)stream>>>(x, gamma, beta, eps, out, rows, n);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { si_set_error(cudaGetErrorString(e)); return SI_ECUDA; }
     return SI_OK;

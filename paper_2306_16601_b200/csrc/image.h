@@ -25,7 +25,9 @@ enum EpiMode : int32_t {
     EPI_REQUANT = 2,     // [REQUANT]              -> 8-bit
     EPI_REQUANT_LUT = 3, // [REQUANT, int chain]   -> 256-entry composite table
     EPI_DEQ_TABLE = 4,   // [DEQ_ACC, f32 unary*, QUANT, int chain] -> breakpoint table over f32
-    EPI_GENERIC = 5      // anything else: device interpreter of _run_chain
+    EPI_GENERIC = 5,     // anything else: device interpreter of _run_chain
+    EPI_DEQ_SIDE = 6     // [DEQ_ACC, ADD_SIDE] -> f32 (residual); kernels run it in their
+                         // EPI_GENERIC instantiation (K2: compiled branch, K1/KREF: interpreter)
 };
 
 struct SiImage {

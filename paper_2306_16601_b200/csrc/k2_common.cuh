@@ -260,6 +260,17 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, i
             v[j] = (int32_t)bp_lookup_bucketed(x, W.s_key, W.s_bkt, W.s_val, E.n_bp, E.bp_key_lo, E.bp_shift,
                                                E.bp_nbucket);
         }
+    } else if (E.mode == EPI_DEQ_SIDE) {
+        // [DEQ_ACC, ADD_SIDE(i)] (residual connection): f32(f64(a) * f64(s))
+        // + side[i][n][m] in f32, the interpreter's two steps without it
+        const float *sd = E.sides + (int64_t)__ldg(E.iparams + 3) * E.N * E.M + m;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const int64_t n = n0 + j;
+            v[j] = (mok && n < P.N)
+                       ? __float_as_int(__fadd_rn(dev_deq_acc((int32_t)(r[j] + (uint32_t)adj), s_in), __ldg(sd + n * E.M)))
+                       : 0;
+        }
     } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {

@@ -225,6 +225,10 @@ Compiled compile_program(const si_program *p)
         c.mode = EPI_DEQ_F32;
         return c;
     }
+    if (L == 2 && p->ops[0] == SI_OP_DEQ_ACC && p->ops[1] == SI_OP_ADD_SIDE && p->out_dtype == SI_F32) {
+        c.mode = EPI_DEQ_SIDE;
+        return c;
+    }
     bool tail_unary = true;
     for (int s = 1; s < L; ++s) tail_unary &= is_unary(p->ops[s]);
     if (p->ops[0] == SI_OP_REQUANT) {

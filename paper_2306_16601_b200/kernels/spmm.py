@@ -167,7 +167,7 @@ def partition_tasks(groups: int, num_bn: int, threads: int) -> tuple:
     return tuple((g0, g1, b0, b1) for b0, b1 in split(num_bn, num_bn) for g0, g1 in granges)
 
 
-_EPI_NAMES = {0: "s32", 1: "deq_f32", 2: "requant", 3: "requant_lut", 4: "deq_table", 5: "generic"}
+_EPI_NAMES = {0: "s32", 1: "deq_f32", 2: "requant", 3: "requant_lut", 4: "deq_table", 5: "generic", 6: "deq_side"}
 
 
 def _build_image(sw: Sparse4x1Weight, program: EpilogueProgram, bias: np.ndarray):

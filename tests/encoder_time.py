@@ -1,0 +1,66 @@
+"""Time the config-4 encoder stack on the GPU box (per-op breakdown of one layer).
+
+    python tests/encoder_time.py [reps]
+"""
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2306_16601_b200.encoder import BertEncoder, EncoderConfig, embeddings, spmm_ops  # noqa: E402
+
+
+def main():
+    reps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
+    cfg = EncoderConfig()
+    t0 = time.perf_counter()
+    enc = BertEncoder(cfg, device="cuda")
+    x = torch.from_numpy(embeddings(cfg, 0)).cuda()
+    enc.calibrate(x)
+    torch.cuda.synchronize()
+    print(f"build + calibrate {time.perf_counter() - t0:.1f} s", flush=True)
+    for _ in range(2):
+        enc.forward(x)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        enc.forward(x)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / reps
+    ops = spmm_ops(cfg)
+    print(f"config4 forward: {ms:.3f} ms  ({cfg.tokens / ms * 1e3:.0f} tokens/s, SpMM effective "
+          f"{ops / ms / 1e9:.1f} TOPS over the whole stack)", flush=True)
+    # per-op breakdown of layer 0 (eager, events around each op)
+    from paper_2306_16601_b200.kernels import relayout_tokens, spmm_exec
+    from paper_2306_16601_b200.kernels import eltwise as E
+    L = enc.layers[0]
+    q = L.quant
+    marks = []
+
+    def mark(name):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        marks.append((name, ev))
+    mark("start")
+    xq = E.quantize_f32(x, q.qp_in); mark("quantize in")
+    qkv = spmm_exec(L.plans["qkv"], relayout_tokens(xq)); mark("spmm qkv 2304x768")
+    ctx = enc._attention(qkv); mark("attention (bmm, softmax, bmm)")
+    cq = E.quantize_f32(ctx, q.qp_ctx); mark("quantize ctx")
+    a = spmm_exec(L.plans["o"], relayout_tokens(cq), sides=x.view(1, cfg.tokens, cfg.hidden)); mark("spmm o +res")
+    h1 = E.layer_norm_f32(a, L.gamma1, L.beta1, cfg.eps); mark("layer norm 1")
+    h1q = E.quantize_f32(h1, q.qp_h1); mark("quantize h1")
+    f = spmm_exec(L.plans["ffn1"], relayout_tokens(h1q)); mark("spmm ffn1 +gelu+quant")
+    g = spmm_exec(L.plans["ffn2"], relayout_tokens(f), sides=h1.view(1, cfg.tokens, cfg.hidden)); mark("spmm ffn2 +res")
+    E.layer_norm_f32(g, L.gamma2, L.beta2, cfg.eps); mark("layer norm 2")
+    torch.cuda.synchronize()
+    for (n0, e0), (n1, e1) in zip(marks, marks[1:]):
+        print(f"  {n1:32s} {e0.elapsed_time(e1) * 1e3:8.1f} us", flush=True)
+
+
+if __name__ == "__main__":
+    main()
