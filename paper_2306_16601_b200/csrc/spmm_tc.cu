@@ -482,8 +482,7 @@ k2m_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
     const int prod = producer_index(warp, 2 + EPI_WARPS);
     const int nprod = (P.debug & 4096) ? 1 : NPROD;   // 4096: single producer (A/B)
     if (prod >= 0) {
-        if (lane == 0) {
-            // ---------------- TMA producers
+        {   // ---------------- TMA producers (whole warp, one elected lane issues)
             const uint32_t full_lead = tc::mapa(tc::smem_u32(full), lead);
             int stage = 0, it = 0;
             uint32_t phase = 0;
@@ -498,17 +497,17 @@ k2m_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
                     tc::mbar_spin(&empty[stage], phase ^ 1);
                     uint8_t *a_s = ring + stage * SLOT;
                     // leader barrier: both W halves + its X half; peer barrier: its X half
-                    tc::mbar_expect_tx(&full[stage], r == 0 ? 2 * P_A + P_B : P_B);
-                    tc::tma_load_2d_2sm(a_s, &tmap_w, full_lead + 8 * stage, mt * 256 + 128 * (int)r, kc * BK);
-                    tc::tma_load_2d_mc(a_s + P_A + q * XROWS * 128, &tmap_x, &full[stage], tok,
+                    tcw::mbar_expect_tx(&full[stage], r == 0 ? 2 * P_A + P_B : P_B);
+                    tcw::tma_load_2d_2sm(a_s, &tmap_w, full_lead + 8 * stage, mt * 256 + 128 * (int)r, kc * BK);
+                    tcw::tma_load_2d_mc(a_s + P_A + q * XROWS * 128, &tmap_x, &full[stage], tok,
                                        kc * BK + (int)q * XROWS, xmask);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && r == 0) {
-            // ---------------- MMA issuer: pair leader, one thread, M256 x N256 x K32
+        if (r == 0) {
+            // ---------------- MMA issuer: pair leader, whole warp, one elected lane issues, M256 x N256 x K32
             const uint32_t idesc = tc::idesc_i8(256, TILE_N, 1, 1);
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
@@ -525,12 +524,12 @@ k2m_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
                     for (int kk = 0; kk < ((P.debug & 16) ? 0 : BK / 32); ++kk) {
                         const uint64_t adesc = tc::smem_desc_sw128(a_addr + kk * 4096, P_A, 1024);
                         const uint64_t bdesc = tc::smem_desc_sw128(b_addr + kk * 4096, P_B, 1024);
-                        tc::mma_i8_2sm(d_tmem, adesc, bdesc, idesc, (kc | kk) ? 1u : 0u);
+                        tcw::mma_i8_2sm(d_tmem, adesc, bdesc, idesc, (kc | kk) ? 1u : 0u);
                     }
-                    tc::mma_commit_2sm_mc(&empty[stage], all_mask);
+                    tcw::mma_commit_2sm_mc(&empty[stage], all_mask);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                tc::mma_commit_2sm_mc(&tfull[acc], pair_mask);
+                tcw::mma_commit_2sm_mc(&tfull[acc], pair_mask);
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }

@@ -422,4 +422,15 @@ __device__ __forceinline__ void tma_load_2d_2sm(void *dst, const CUtensorMap *m,
         ::"r"(tc::smem_u32(dst)), "l"((uint64_t)m), "r"(c0), "r"(c1), "r"(leader_bar)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_2d_mc(void *dst, const CUtensorMap *m, uint64_t *bar, int32_t c0, int32_t c1,
+                                               uint16_t cta_mask)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 r;\n\t"
+        "elect.sync r|p, 0xffffffff;\n\t"
+        "@p cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3}], [%4], %5;\n}"
+        ::"r"(tc::smem_u32(dst)), "l"((uint64_t)m), "r"(c0), "r"(c1), "r"(tc::smem_u32(bar)), "h"(cta_mask)
+        : "memory");
+}
 }  // namespace tcw
