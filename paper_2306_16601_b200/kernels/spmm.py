@@ -179,10 +179,15 @@ def _build_image(sw: Sparse4x1Weight, program: EpilogueProgram, bias: np.ndarray
     image = np.zeros(size.value, dtype=np.uint8)
     _lib.check(L.si_plan_image_build(ctypes.byref(hw.s), ctypes.byref(hp.s), _lib.ptr(bias),
                                      _lib.ptr(image), size.value), "plan_spmm")
+    return image, plan_info(image)
+
+
+def plan_info(image: np.ndarray) -> dict:
+    """Header summary of a plan image (si_plan_info_get); raises on an image
+    whose magic / version this library does not know."""
     info = _lib.SiPlanInfo()
-    _lib.check(L.si_plan_info_get(_lib.ptr(image), ctypes.byref(info)), "plan_spmm")
-    return image, {f: getattr(info, f) for f, _ in info._fields_} | {
-        "epilogue": _EPI_NAMES.get(info.epi_mode, "?")}
+    _lib.check(_lib.lib().si_plan_info_get(_lib.ptr(image), ctypes.byref(info)), "plan image")
+    return {f: getattr(info, f) for f, _ in info._fields_} | {"epilogue": _EPI_NAMES.get(info.epi_mode, "?")}
 
 
 def plan_spmm(sw: Sparse4x1Weight, n: int, threads: int = 1, program: EpilogueProgram | None = None,
