@@ -15,7 +15,7 @@
 #endif
 
 #define SI_IMG_MAGIC 0x58344953u /* "SI4X" */
-#define SI_IMG_VERSION 3u
+#define SI_IMG_VERSION 4u
 #define TR_SLOTS 128 /* K2t residual slots per 256-row pair tile */
 
 // compiled epilogue forms (see plan.cpp: compile_program)
@@ -97,7 +97,7 @@ struct SiImage {
     uint64_t off_tr_k;       // u16   [pairs][TR_SLOTS]   activation column of each slot
     uint64_t off_tr_cnt;     // i32   [pairs]             residual MMAs (64 slots each; 0..TR_SLOTS/64)
     int32_t tr_ok, tr_pairs; // tr_ok 0: some pair tile needs more than TR_SLOTS slots (K2t unavailable)
-    uint64_t reserved5;
+    uint64_t off_tc_wrow;    // int8  [tc_mtiles*128][tc_kpad] dense W row-major (K2a: rows loaded into TMEM)
 };
 
 static_assert(sizeof(SiImage) % 16 == 0, "image header must stay 16-byte aligned");

@@ -102,14 +102,22 @@ struct EpiWarp {
 // One 32-token chunk of one warp: TMEM columns -> outputs.  m is this
 // lane's weight row, n0 the chunk's first token, c the chunk index within the
 // warp's 64 columns (staging row offset).
-template <int MODE, int OUTK, bool RES = false>
+struct NoOp {
+    __device__ __forceinline__ void operator()() const {}
+};
+
+// on_loaded() runs once the chunk's accumulators are in registers (K2a
+// releases the TMEM accumulator there, before the math and the stores).
+template <int MODE, int OUTK, bool RES = false, typename OnLoaded = NoOp>
 __device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, int32_t adj, float s_in, float cq,
                                           float gm, bool fast, int64_t n0, int c, const K2Params &P,
-                                          const EpiParams &E, const EpiWarp &W, int32_t rp0 = 0, int32_t rp1 = 0)
+                                          const EpiParams &E, const EpiWarp &W, int32_t rp0 = 0, int32_t rp1 = 0,
+                                          OnLoaded on_loaded = OnLoaded())
 {
     uint32_t r[32];
     tc::tmem_ld_32x32b_x32(taddr, r);
     tc::tmem_ld_wait();
+    on_loaded();
     if constexpr (RES) {
         // K2s: block columns that did not fit the 2:4 operand (windows with
         // more than two nonzero columns), w * X[k][n0 .. n0+31] per entry
@@ -490,6 +498,24 @@ bool encode_2d(CUtensorMap *m, const void *ptr, uint64_t inner, uint64_t outer, 
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(ptr), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// 3-D view for a token-major [N][K] activation: dims {128 (k in block), N,
+// K/128 (block)}, so one box of {128, rows, blocks} lands as `blocks`
+// consecutive K-major SWIZZLE_128B tiles of `rows` x 128 B.  Needs K % 128 == 0.
+bool encode_3d_kblocks(CUtensorMap *m, const void *ptr, uint64_t n, uint64_t k, uint64_t pitch_bytes, uint32_t rows,
+                       uint32_t blocks)
+{
+    EncodeTiledFn enc = encode_fn();
+    if (!enc || k % 128) return false;
+    cuuint64_t dims[3] = {128, n, k / 128};
+    cuuint64_t strides[2] = {pitch_bytes, 128};
+    cuuint32_t box[3] = {128, rows, blocks};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void *>(ptr), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }

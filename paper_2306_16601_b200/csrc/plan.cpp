@@ -271,7 +271,7 @@ Compiled compile_program(const si_program *p)
 }
 
 struct Layout {
-    uint64_t off[28];
+    uint64_t off[29];
     uint64_t total;
 };
 
@@ -693,6 +693,7 @@ static Layout make_layout(const si_weight *w, const si_program *p, const Compile
     put(25, sp.tr_img.size());
     put(26, 2 * sp.tr_k.size());
     put(27, 4 * sp.tr_cnt.size());
+    put(28, (uint64_t)kp * ((mt + 1) / 2 * 2) * 128);   // whole 256-row pair tiles
     l.total = cur;
     return l;
 }
@@ -755,6 +756,7 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
     h->off_tr_cnt = l.off[27];
     h->tr_ok = sp.tr_ok;
     h->tr_pairs = (int32_t)sp.tr_cnt.size();
+    h->off_tc_wrow = l.off[28];
     std::memcpy(base + h->off_tr_img, sp.tr_img.data(), sp.tr_img.size());
     std::memcpy(base + h->off_tr_k, sp.tr_k.data(), 2 * sp.tr_k.size());
     std::memcpy(base + h->off_tr_cnt, sp.tr_cnt.data(), 4 * sp.tr_cnt.size());
@@ -879,6 +881,11 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
                 int8_t v = w->vals[(q / 4) * 16 + r * 4 + (q % 4)];
                 if (m < M && v) wt[(int64_t)w->idx[q] * ldm + m] += v;
             }
+    // K2a source: the same dense W, row-major [mtiles*128][kpad] (k contiguous)
+    int8_t *wr = (int8_t *)(base + h->off_tc_wrow);
+    const int64_t kpad = h->tc_kpad;
+    for (int64_t k = 0; k < kpad; ++k)
+        for (int64_t m = 0; m < ldm; ++m) wr[m * kpad + k] = wt[k * ldm + m];
     return SI_OK;
 }
 

@@ -1189,8 +1189,12 @@ int k2_launch(const SpmmArgs &a)
         return s == "single" ? (int)V_SINGLE : s == "pair" ? (int)V_PAIR : s == "xstat" ? (int)V_PAIR_XSTAT
              : s == "expand" ? (int)V_EXPAND : s == "expand_xstat" ? (int)V_EXPAND_XSTAT
              : s == "sparse" ? (int)V_SPARSE : s == "mc2" ? (int)V_MC2 : s == "mc4" ? (int)V_MC4
-             : s == "pair256" ? (int)V_PAIR256 : s == "xsparse" ? 100 : -1;
+             : s == "pair256" ? (int)V_PAIR256 : s == "xsparse" ? 100 : s == "tmemw" ? 101 : -1;
     }();
+    if (forced == 101) {
+        if (k2a_supported(h, a.n, a.layout, a.x, a.ldx)) return k2a_launch(a);
+        return (int)cudaErrorInvalidValue;
+    }
     // K2t (X-stationary 2:4, spmm_tcx.cu; SI_K2_VARIANT=xsparse): token-major
     // X, K <= 1024, every pair tile's residual fits its slots.  Opt-in: on the
     // config-5 shapes it measures slower than the dense pair.

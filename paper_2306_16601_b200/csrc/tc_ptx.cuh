@@ -158,6 +158,27 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap *m, const void *s
                  : "memory");
 }
 __device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// L2 eviction-priority policies for the TMA cache-hint forms
+__device__ __forceinline__ uint64_t policy_evict_first()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// TMA store with an L2 cache hint (outputs streamed past L2: evict_first)
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap *m, const void *src, int32_t c0, int32_t c1,
+                                                  uint64_t policy)
+{
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;"
+                 ::"l"((uint64_t)m), "r"(smem_u32(src)), "r"(c0), "r"(c1), "l"(policy)
+                 : "memory");
+}
 __device__ __forceinline__ void tma_store_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void tma_store_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void tma_store_wait_all0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -431,6 +452,36 @@ __device__ __forceinline__ void tma_load_2d_mc(void *dst, const CUtensorMap *m, 
         "@p cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
         " [%0], [%1, {%2, %3}], [%4], %5;\n}"
         ::"r"(tc::smem_u32(dst)), "l"((uint64_t)m), "r"(c0), "r"(c1), "r"(tc::smem_u32(bar)), "h"(cta_mask)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_2sm(void *dst, const CUtensorMap *m, uint32_t leader_bar, int32_t c0,
+                                                int32_t c1, int32_t c2)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 r;\n\t"
+        "elect.sync r|p, 0xffffffff;\n\t"
+        "@p cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n}"
+        ::"r"(tc::smem_u32(dst)), "l"((uint64_t)m), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_2sm_hint(void *dst, const CUtensorMap *m, uint32_t leader_bar, int32_t c0,
+                                                     int32_t c1, uint64_t policy)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 r;\n\t"
+        "elect.sync r|p, 0xffffffff;\n\t"
+        "@p cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;\n}"
+        ::"r"(tc::smem_u32(dst)), "l"((uint64_t)m), "r"(c0), "r"(c1), "r"(leader_bar), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_2sm_hint(void *dst, const CUtensorMap *m, uint32_t leader_bar, int32_t c0,
+                                                     int32_t c1, int32_t c2, uint64_t policy)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 r;\n\t"
+        "elect.sync r|p, 0xffffffff;\n\t"
+        "@p cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;\n}"
+        ::"r"(tc::smem_u32(dst)), "l"((uint64_t)m), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar), "l"(policy)
         : "memory");
 }
 }  // namespace tcw

@@ -67,7 +67,7 @@ class SiImageHeader(_ct.Structure):
                 ("off_sp_rptr", _ct.c_uint64), ("off_sp_res", _ct.c_uint64), ("sp_nres", _ct.c_int32),
                 ("sp_maxres", _ct.c_int32), ("off_rqp", _ct.c_uint64), ("off_tr_img", _ct.c_uint64),
                 ("off_tr_k", _ct.c_uint64), ("off_tr_cnt", _ct.c_uint64), ("tr_ok", _ct.c_int32),
-                ("tr_pairs", _ct.c_int32), ("reserved5", _ct.c_uint64)]
+                ("tr_pairs", _ct.c_int32), ("off_tc_wrow", _ct.c_uint64)]
 
 
 def image_header(img: np.ndarray) -> SiImageHeader:

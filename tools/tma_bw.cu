@@ -11,6 +11,10 @@
 __global__ void tma_bw_kernel(const __grid_constant__ CUtensorMap tm, int S, int box_rows, int iters, int rows_total,
                               int stride_ctas, int nprod, int ncols)
 {
+    // nprod >= 1000: warp-converged producers (whole warp loops, one elected
+    // lane issues, tcw::), nprod - 1000 of them
+    const bool conv = nprod >= 1000;
+    if (conv) nprod -= 1000;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
     const int slot_bytes = box_rows * 128;
@@ -24,13 +28,14 @@ __global__ void tma_bw_kernel(const __grid_constant__ CUtensorMap tm, int S, int
     __syncthreads();
     const int nboxes = rows_total / box_rows;
     const int w = threadIdx.x >> 5;
-    if (w >= 2 && w < 2 + (nprod < 0 ? -nprod : nprod) && (threadIdx.x & 31) == 0) {
+    if (w >= 2 && w < 2 + (nprod < 0 ? -nprod : nprod) && (conv || (threadIdx.x & 31) == 0)) {
         // producer p issues iterations i = p, p + nprod, ... (slot i % S)
         for (int i = w - 2; i < iters; i += (nprod < 0 ? -nprod : nprod)) {
             const int stage = i % S;
             const uint32_t phase = (uint32_t)((i / S) & 1);
             tc::mbar_spin(&empty[stage], phase ^ 1);
-            tc::mbar_expect_tx(&full[stage], slot_bytes);
+            if (conv) tcw::mbar_expect_tx(&full[stage], slot_bytes);
+            else tc::mbar_expect_tx(&full[stage], slot_bytes);
             int b, col;
             if (stride_ctas == 0) {
                 // disjoint: CTA c streams its own slice of the buffer
@@ -42,7 +47,8 @@ __global__ void tma_bw_kernel(const __grid_constant__ CUtensorMap tm, int S, int
                 b = (int)(q & (unsigned)(nboxes - 1));
                 col = (int)((q >> 4) & (unsigned)(ncols - 1));
             }
-            tc::tma_load_2d(smem + stage * slot_bytes, &tm, &full[stage], col * 128, b * box_rows);
+            if (conv) tcw::tma_load_2d(smem + stage * slot_bytes, &tm, &full[stage], col * 128, b * box_rows);
+            else tc::tma_load_2d(smem + stage * slot_bytes, &tm, &full[stage], col * 128, b * box_rows);
         }
     } else if (threadIdx.x == 32) {
         int stage = 0;
@@ -81,12 +87,13 @@ extern "C" double tma_bw(const void *buf, long rows_total, int S, int box_rows, 
     const int smem = S * box_rows * 128 + 1024 + 2048;
     if (cudaFuncSetAttribute(tma_bw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
         return -3;
-    tma_bw_kernel<<<ctas, 64 + 32 * (nprod < 0 ? -nprod : nprod), smem>>>(tm, S, box_rows, iters, (int)rows_total, stride_ctas, nprod, ncols);
+    const int np = nprod >= 1000 ? nprod - 1000 : (nprod < 0 ? -nprod : nprod);
+    tma_bw_kernel<<<ctas, 64 + 32 * np, smem>>>(tm, S, box_rows, iters, (int)rows_total, stride_ctas, nprod, ncols);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a);
-    for (int r = 0; r < reps; ++r) tma_bw_kernel<<<ctas, 64 + 32 * (nprod < 0 ? -nprod : nprod), smem>>>(tm, S, box_rows, iters, (int)rows_total, stride_ctas, nprod, ncols);
+    for (int r = 0; r < reps; ++r) tma_bw_kernel<<<ctas, 64 + 32 * np, smem>>>(tm, S, box_rows, iters, (int)rows_total, stride_ctas, nprod, ncols);
     cudaEventRecord(b);
     if (cudaEventSynchronize(b) != cudaSuccess) return -4;
     float ms = 0;

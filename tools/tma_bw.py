@@ -14,18 +14,20 @@ def build():
                     "-Xcompiler", "-fPIC", "-o", SO, os.path.join(HERE, "tma_bw.cu")], check=True)
 
 
-def producer_sweep():
-    """Per-SM TMA throughput vs producer warps and box size (148 CTAs, S slots)."""
+def producer_sweep(conv=False):
+    """Per-SM TMA throughput vs producer warps and box size (148 CTAs, S slots);
+    conv: warp-converged producers (tcw::) instead of lone lane-0 threads."""
     L = ctypes.CDLL(SO)
     L.tma_bw.restype = ctypes.c_double
     L.tma_bw.argtypes = [ctypes.c_void_p, ctypes.c_long] + [ctypes.c_int] * 7 + [ctypes.c_long]
     buf = torch.randint(0, 255, (96 << 20,), dtype=torch.uint8, device="cuda")
     rows = (96 << 20) // 128
-    for box in (96, 128, 192, 256):
-        for nprod in (1, 2, 4, 8):
+    for box in (64, 96, 128, 256):
+        for nprod in (1, 2, 4):
             S = max(2, min(16, (192 * 1024) // (box * 128)))
-            bw = L.tma_bw(buf.data_ptr(), rows, S, box, 2048, 148, 0, 5, nprod, 128) / 148
-            print(f"box {box * 128 // 1024:2d} KB S {S:2d} producers {nprod}: {bw:6.1f} GB/s per SM", flush=True)
+            bw = L.tma_bw(buf.data_ptr(), rows, S, box, 2048, 148, 0, 5, nprod + (1000 if conv else 0), 128) / 148
+            print(f"box {box * 128 // 1024:2d} KB S {S:2d} producers {nprod}{' (converged)' if conv else ''}: "
+                  f"{bw:6.1f} GB/s per SM", flush=True)
 
 
 def commit_sweep():
@@ -122,7 +124,7 @@ if __name__ == "__main__":
         pair_sweep()
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "prod":
-        producer_sweep()
+        producer_sweep(conv=len(sys.argv) > 2)
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "lat":
         latency_sweep()
