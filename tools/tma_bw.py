@@ -89,6 +89,20 @@ def pair_small():
                   f"{bw:6.1f} GB/s per SM", flush=True)
 
 
+def pitch_sweep():
+    """Box rows contiguous (pitch 128 B) vs strided like the kernels' operand
+    tiles (X [N][K] rows K bytes apart, [K][N] rows N bytes apart)."""
+    L = ctypes.CDLL(SO)
+    L.tma_bw.restype = ctypes.c_double
+    L.tma_bw.argtypes = [ctypes.c_void_p, ctypes.c_long] + [ctypes.c_int] * 7 + [ctypes.c_long]
+    buf = torch.randint(0, 255, (96 << 20,), dtype=torch.uint8, device="cuda")
+    for pitch in (128, 1024, 4096, 65536):
+        rows = (96 << 20) // pitch
+        for box, S in ((64, 16), (128, 12)):
+            bw = L.tma_bw(buf.data_ptr(), rows, S, box, 2048, 148, 0, 5, 4, pitch) / 148
+            print(f"pitch {pitch:6d} B, box {box} rows x 128 B, S {S}, 4 producers: {bw:6.1f} GB/s per SM", flush=True)
+
+
 def latency_sweep():
     """Per-SM TMA throughput vs ring depth, 1 CTA vs 148 CTAs (disjoint L2-resident
     slices): the implied round trip S * box / (bytes/s per SM)."""
@@ -116,6 +130,9 @@ if __name__ == "__main__":
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "shared":
         shared_sweep()
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "pitch":
+        pitch_sweep()
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "pairsmall":
         pair_small()
