@@ -28,9 +28,12 @@ int32_t pick_kernel(const SiImage *h, int64_t n, int32_t layout, int32_t kernel,
                     int64_t ldo)
 {
     if (kernel != SI_KERNEL_AUTO) return kernel;
-    // tensor cores once the token tile is worth a 128-row MMA tile; the
-    // crossover is measured
-    if (n >= 1024 && k2_supported(h, n, layout, x, ldx, ldo)) return SI_KERNEL_TC;
+    // tensor cores whenever TMA-legal, except tiny weights at small N where
+    // the gather kernel's single wave is shorter; measured over all 140
+    // config-2 cells with CUDA-graph replay (profiles/r01b_config2_*.md,
+    // DESIGN.md "Kernel selection")
+    if ((n >= 1024 || (int64_t)h->M * h->K >= (1 << 18)) && k2_supported(h, n, layout, x, ldx, ldo))
+        return SI_KERNEL_TC;
     return SI_KERNEL_GATHER;
 }
 

@@ -234,3 +234,30 @@ def test_host_batch_entry_point():
     outs = K.spmm_exec_host_batch(items, chunk=2048)
     for i, (o, (ref, prog)) in enumerate(zip(outs, want)):
         check_equal(o.numpy(), ref, prog, ("batch job", i))
+
+
+_C2_CACHE = {}
+
+
+def _c2_weight(cell):
+    key = (cell.m, cell.k, cell.ratio, cell.seed)
+    if key not in _C2_CACHE:
+        w, _, bias, scales = baseline_inputs(cell.m, cell.k, 1, cell.ratio, cell.seed)
+        _C2_CACHE[key] = (w, P.encode_sparse(w, scales), bias, scales)
+    return _C2_CACHE[key]
+
+
+@pytest.mark.parametrize("cell", workloads.config2_cells(), ids=lambda c: c.name)
+def test_config2_sweep_cell(cell):
+    """BASELINE config 2: every (M, K) x N x sparsity cell with the f32
+    dequant epilogue on the GPU; the oracle on the first and last 128 tokens
+    (bit-exact f32)."""
+    w, sw, bias, scales = _c2_weight(cell)
+    x = np.random.default_rng(cell.seed + 1).integers(0, 256, (cell.k, cell.n), dtype=np.uint8)
+    prog = workloads.program(cell.program, scales)
+    got = run(sw, x, prog, bias)
+    assert got.shape == (cell.n, cell.m)
+    for s0 in sorted({0, max(cell.n - 128, 0)}):
+        xs = np.ascontiguousarray(x[:, s0: s0 + 128])
+        want = oracle.spmm_exec(sw, xs, prog, bias)
+        check_equal(got[s0: s0 + 128], want, prog, (cell.name, s0))
