@@ -484,4 +484,14 @@ __device__ __forceinline__ void tma_load_3d_2sm_hint(void *dst, const CUtensorMa
         ::"r"(tc::smem_u32(dst)), "l"((uint64_t)m), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar), "l"(policy)
         : "memory");
 }
+// L2 prefetch of one tensor box (no smem, no barrier)
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *m, int32_t c0, int32_t c1)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 r;\n\t"
+        "elect.sync r|p, 0xffffffff;\n\t"
+        "@p cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n}"
+        ::"l"((uint64_t)m), "r"(c0), "r"(c1)
+        : "memory");
+}
 }  // namespace tcw
