@@ -42,7 +42,7 @@ struct EpiParams {
     int64_t N;
     const int32_t *bp_key;
     const uint16_t *bp_bucket;
-    int32_t bp_key_lo, bp_shift, bp_nbucket;
+    int32_t bp_key_lo, bp_shift, bp_nbucket, bp_occ;
 };
 
 static inline EpiParams make_epi(const SiImage *h, const void *img, const float *sides, int64_t n)
@@ -76,6 +76,7 @@ static inline EpiParams make_epi(const SiImage *h, const void *img, const float 
     e.bp_key_lo = h->bp_key_lo;
     e.bp_shift = h->bp_shift;
     e.bp_nbucket = h->bp_nbucket;
+    e.bp_occ = h->bp_occ;
     return e;
 }
 
@@ -188,6 +189,29 @@ __device__ __forceinline__ uint32_t bp_lookup_bucketed(float x, const int32_t *k
     b = min(b, (uint32_t)(nbucket - 1));
     int i = bucket[b];
     while (i < n && keys[i] <= k) ++i;
+    return vals[i];
+}
+
+// The same lookup as a fixed-length branchless binary search inside the
+// bucket: the answer lies in [bucket[b], bucket[b] + occ] (occ = the most
+// thresholds any bucket holds, plan.cpp), so S steps with 2^S > occ find it.
+// Every lane runs the same straight-line code: the 32 lookups of an epilogue
+// chunk neither diverge nor loop.
+template <int S>
+__device__ __forceinline__ uint32_t bp_lookup_fixed(float x, const int32_t *keys, const uint16_t *bucket,
+                                                    const uint32_t *vals, int n, int32_t key_lo, int shift,
+                                                    int nbucket)
+{
+    const int32_t k = f32_key(x);
+    const uint32_t d = k < key_lo ? 0u : (uint32_t)k - (uint32_t)key_lo;
+    const uint32_t b = min(d >> shift, (uint32_t)(nbucket - 1));
+    int i = bucket[b];
+#pragma unroll
+    for (int st = 1 << (S - 1); st >= 1; st >>= 1) {
+        const int j = i + st;   // take the step if keys[j - 1] <= k
+        const int32_t kk = keys[min(j, n) - 1];
+        i = (j <= n && kk <= k) ? j : i;
+    }
     return vals[i];
 }
 

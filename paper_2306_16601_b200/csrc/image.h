@@ -63,7 +63,7 @@ struct SiImage {
     uint64_t total_bytes;
     uint64_t off_rqc;        // f32   [M]               f32(f64(scale_in)/f64(fp)) for the requant fast path
     // bucketed index over the breakpoint thresholds (f32 total-order keys)
-    int32_t bp_key_lo, bp_shift, bp_nbucket, pad2;
+    int32_t bp_key_lo, bp_shift, bp_nbucket, bp_occ;   // bp_occ: most thresholds in one bucket
     uint64_t off_bp_key;     // i32   [n_bp]            threshold keys
     uint64_t off_bp_bucket;  // u16   [bp_nbucket]      first threshold index per key bucket
     // K2 on-chip expansion lists: for every (128-row tile rt, 128-k chunk kc,

@@ -262,12 +262,31 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, i
             }
         }
     } else if constexpr (MODE == EPI_DEQ_TABLE) {
+        // (uniform branch on the plan's bucket occupancy) fixed-step lookups
+#define SI_BP_CHUNK(S)                                                                                          \
+    for (int j = 0; j < 32; ++j) {                                                                              \
+        const float x = dev_deq_acc((int32_t)(r[j] + (uint32_t)adj), s_in);                                    \
+        v[j] = (int32_t)bp_lookup_fixed<S>(x, W.s_key, W.s_bkt, W.s_val, E.n_bp, E.bp_key_lo, E.bp_shift,        \
+                                           E.bp_nbucket);                                                       \
+    }
+        if (E.n_bp > 0 && E.bp_occ < 4) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            const float x = dev_deq_acc((int32_t)(r[j] + (uint32_t)adj), s_in);
-            v[j] = (int32_t)bp_lookup_bucketed(x, W.s_key, W.s_bkt, W.s_val, E.n_bp, E.bp_key_lo, E.bp_shift,
-                                               E.bp_nbucket);
+            SI_BP_CHUNK(2)
+        } else if (E.n_bp > 0 && E.bp_occ < 16) {
+#pragma unroll
+            SI_BP_CHUNK(4)
+        } else if (E.n_bp > 0 && E.bp_occ < 64) {
+#pragma unroll
+            SI_BP_CHUNK(6)
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const float x = dev_deq_acc((int32_t)(r[j] + (uint32_t)adj), s_in);
+                v[j] = (int32_t)bp_lookup_bucketed(x, W.s_key, W.s_bkt, W.s_val, E.n_bp, E.bp_key_lo, E.bp_shift,
+                                                   E.bp_nbucket);
+            }
         }
+#undef SI_BP_CHUNK
     } else if (E.mode == EPI_DEQ_SIDE) {
         // [DEQ_ACC, ADD_SIDE(i)] (residual connection): f32(f64(a) * f64(s))
         // + side[i][n][m] in f32, the interpreter's two steps without it

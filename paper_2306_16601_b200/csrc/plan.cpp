@@ -184,7 +184,7 @@ struct Compiled {
     int32_t q_zp = 0, q_lo = 0, q_hi = 0;
     std::vector<uint32_t> clut;
     BpTable bp;
-    int32_t bp_key_lo = 0, bp_shift = 0;
+    int32_t bp_key_lo = 0, bp_shift = 0, bp_occ = 0;
     std::vector<uint16_t> bp_bucket;
 };
 
@@ -209,6 +209,15 @@ void build_buckets(Compiled &c)
         while (i < n && f2key(c.bp.x[i]) < start) ++i;
         c.bp_bucket[(size_t)b] = (uint16_t)i;
     }
+    // most thresholds any bucket holds: a lookup never advances further than
+    // that from bucket[b], so the device can take a fixed, divergence-free
+    // number of steps
+    int32_t occ = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        const int64_t next = b + 1 < nb ? c.bp_bucket[(size_t)b + 1] : (int64_t)n;
+        occ = std::max<int32_t>(occ, (int32_t)(next - c.bp_bucket[(size_t)b]));
+    }
+    c.bp_occ = occ;
 }
 
 Compiled compile_program(const si_program *p)
@@ -743,6 +752,7 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
     h->off_bp_bucket = l.off[17];
     h->bp_key_lo = c.bp_key_lo;
     h->bp_shift = c.bp_shift;
+    h->bp_occ = c.bp_occ;
     h->bp_nbucket = (int32_t)c.bp_bucket.size();
     h->off_rqg = l.off[20];
     h->off_sp_img = l.off[21];

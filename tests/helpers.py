@@ -61,7 +61,7 @@ class SiImageHeader(_ct.Structure):
                                             "off_chans", "off_clut", "off_bp_x", "off_bp_v", "off_tc_wt",
                                             "total_bytes", "off_rqc")] + \
                [("bp_key_lo", _ct.c_int32), ("bp_shift", _ct.c_int32), ("bp_nbucket", _ct.c_int32),
-                ("pad2", _ct.c_int32), ("off_bp_key", _ct.c_uint64), ("off_bp_bucket", _ct.c_uint64),
+                ("bp_occ", _ct.c_int32), ("off_bp_key", _ct.c_uint64), ("off_bp_bucket", _ct.c_uint64),
                 ("tc_emax", _ct.c_int32), ("tc_nlists", _ct.c_int32), ("off_tc_eptr", _ct.c_uint64),
                 ("off_tc_ent", _ct.c_uint64), ("off_rqg", _ct.c_uint64), ("off_sp_img", _ct.c_uint64),
                 ("off_sp_rptr", _ct.c_uint64), ("off_sp_res", _ct.c_uint64), ("sp_nres", _ct.c_int32),
