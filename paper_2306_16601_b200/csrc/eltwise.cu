@@ -136,10 +136,28 @@ __global__ void k_layer_norm_rows(const float *x, const float *gamma, const floa
 __device__ __forceinline__ void load_rows(const float *x, int64_t ld, int64_t rows, int64_t r0, int n, float *t)
 {
     const int lane = threadIdx.x & 31;
-    for (int r = 0; r < ROWS; ++r) {
-        const int64_t row = r0 + r;
+    if ((n & 3) == 0 && (ld & 3) == 0 && (((uintptr_t)x) & 15) == 0) {
+        // 16-byte loads, 8 rows in flight per lane (the load phase is latency-bound)
+        const int n4 = n >> 2;
+        for (int r0i = 0; r0i < ROWS; r0i += 8) {
+#pragma unroll
+            for (int rr = 0; rr < 8; ++rr) {
+                const int r = r0i + rr;
+                const int64_t row = r0 + r;
+                for (int c4 = lane; c4 < n4; c4 += 32) {
+                    const float4 v = row < rows ? __ldg(reinterpret_cast<const float4 *>(x + row * ld) + c4)
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+                    float *d = t + r * (n + 1) + 4 * c4;
+                    d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+                }
+            }
+        }
+    } else {
+        for (int r = 0; r < ROWS; ++r) {
+            const int64_t row = r0 + r;
 #pragma unroll 4
-        for (int c = lane; c < n; c += 32) t[r * (n + 1) + c] = row < rows ? x[row * ld + c] : 0.0f;
+            for (int c = lane; c < n; c += 32) t[r * (n + 1) + c] = row < rows ? x[row * ld + c] : 0.0f;
+        }
     }
     __syncwarp();
 }
@@ -147,6 +165,18 @@ __device__ __forceinline__ void store_rows(float *out, int64_t ld, int64_t rows,
 {
     const int lane = threadIdx.x & 31;
     __syncwarp();
+    if ((n & 3) == 0 && (ld & 3) == 0 && (((uintptr_t)out) & 15) == 0) {
+        const int n4 = n >> 2;
+        for (int r = 0; r < ROWS; ++r) {
+            const int64_t row = r0 + r;
+            if (row >= rows) break;
+            for (int c4 = lane; c4 < n4; c4 += 32) {
+                const float *sv = t + r * (n + 1) + 4 * c4;
+                reinterpret_cast<float4 *>(out + row * ld)[c4] = make_float4(sv[0], sv[1], sv[2], sv[3]);
+            }
+        }
+        return;
+    }
     for (int r = 0; r < ROWS; ++r) {
         const int64_t row = r0 + r;
         if (row >= rows) break;

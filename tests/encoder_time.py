@@ -49,7 +49,16 @@ def main():
     mark("start")
     xq = E.quantize_f32(x, q.qp_in); mark("quantize in")
     qkv = spmm_exec(L.plans["qkv"], relayout_tokens(xq)); mark("spmm qkv 2304x768")
-    ctx = enc._attention(qkv); mark("attention (bmm, softmax, bmm)")
+    # attention, op by op (the composition of BertEncoder._attention)
+    B, S, H, nh = cfg.batch, cfg.seq, cfg.hidden, cfg.heads
+    d, ld = H // nh, 3 * H
+    scores = torch.empty((B, nh, S, S), dtype=torch.float32, device="cuda")
+    E.bmm_strided(qkv, qkv[:, H:], scores, B, nh, S, d, S, (S * ld, d, ld), (S * ld, d, ld),
+                  (nh * S * S, S * S, S), True, E.attention_scale(d)); mark("  scores bmm (NT)")
+    E.softmax_f32(scores, out=scores); mark("  softmax")
+    ctx = torch.empty((B * S, H), dtype=torch.float32, device="cuda")
+    E.bmm_strided(scores, qkv[:, 2 * H:], ctx, B, nh, S, S, d, (nh * S * S, S * S, S), (S * ld, d, ld),
+                  (S * H, d, H), False, 1.0); mark("  context bmm (NN)")
     cq = E.quantize_f32(ctx, q.qp_ctx); mark("quantize ctx")
     a = spmm_exec(L.plans["o"], relayout_tokens(cq), sides=x.view(1, cfg.tokens, cfg.hidden)); mark("spmm o +res")
     h1 = E.layer_norm_f32(a, L.gamma1, L.beta1, cfg.eps); mark("layer norm 1")
