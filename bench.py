@@ -171,6 +171,10 @@ def main():
     ap.add_argument("--e2e-chunk", type=int, default=32768, help="token chunk of the host pipeline")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--shard", default="tokens", choices=["tokens", "rows"],
+                    help="tokens: each rank its own 65536 tokens, no collective (weak scaling); rows: the weight "
+                         "rows of every linear split over the ranks, one NCCL all-gather of the u8 outputs per "
+                         "linear (strong scaling, SURVEY 8(e))")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -189,17 +193,25 @@ def main():
     cells = make_cells()
     n = cells[0].n
 
+    rows_mode = args.shard == "rows"
+    if rows_mode:
+        args.no_graphs = True   # the step holds NCCL collectives: eager launches
     # ---- setup (outside the timed region): plans, inputs in HBM, outputs
     layers = []
     for c in cells:
-        w, x, bias, scales = workloads.baseline_inputs(c.m, c.k, n, c.ratio, c.seed + 1000 * rank)
+        # rows mode: every rank holds the same tokens and computes its row shard
+        w, x, bias, scales = workloads.baseline_inputs(c.m, c.k, n, c.ratio, c.seed + (0 if rows_mode else 1000 * rank))
         sw = P.encode_sparse(w, scales)
         prog = workloads.program(c.program, scales)
         plan = K.plan_spmm(sw, n, program=prog, bias=bias, device=dev)
         act = K.relayout_activation(torch.from_numpy(x).pin_memory(), device=dev)
         out = torch.empty((n, c.m), dtype=torch.uint8, device=dev)
+        rs = None
+        if rows_mode:
+            from paper_2306_16601_b200.parallel import RowShardedSpmm
+            rs = RowShardedSpmm(sw, n, prog, bias=bias, device=dev) if world > 1 else None
         layers.append(dict(cell=c, sw=sw, x_host=torch.from_numpy(x).pin_memory(), plan=plan, act=act,
-                           out=out, prog=prog, bias=bias))
+                           out=out, prog=prog, bias=bias, rows=rs))
         del x
     stream = torch.cuda.current_stream(dev)
     launches_per_step = sum(
@@ -214,6 +226,8 @@ def main():
                 evs[i][0].record(stream)
             if graphs:
                 graphs[i].replay()
+            elif L["rows"] is not None:
+                L["out"] = L["rows"].run(L["act"], kernel=args.kernel)
             else:
                 K.spmm_exec(L["plan"], L["act"], out=L["out"], kernel=args.kernel)
             if evs is not None:
@@ -255,7 +269,9 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     ops_step = sum(L["cell"].ops(n) for L in layers)
-    value = ops_step * world * args.steps / (ms_max / 1e3) / 1e12
+    # tokens: every rank did a full step on its own tokens; rows: the ranks
+    # shared one step's work
+    value = ops_step * (1 if rows_mode else world) * args.steps / (ms_max / 1e3) / 1e12
 
     # per-linear kernel durations -> roofline of the dominant kernel
     layer_ms = [float(np.mean([per_layer[s][i][0].elapsed_time(per_layer[s][i][1]) for s in range(args.steps)]))
@@ -299,6 +315,7 @@ def main():
     te = torch.tensor([float(np.mean(e2e_ms))], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    # (rows mode: the host-buffer path runs each rank's full linears unsharded)
     e2e_value = ops_step * world / (float(te.item()) / 1e3) / 1e12
 
     cpu = None
@@ -309,12 +326,14 @@ def main():
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8xs8->s32", "data": "synthetic",
+            "scaling": "strong" if rows_mode else "weak", "vs_baseline": None, "dtype": "u8xs8->s32",
+            "data": "synthetic",
             "config": {"workload": "config5_bert_large_spmm_set", "tokens_per_rank": n,
-                       "global_tokens": n * world, "linears": [c.name for c in cells], "sparsity": 0.9,
+                       "global_tokens": n if rows_mode else n * world, "linears": [c.name for c in cells], "sparsity": 0.9,
                        "epilogue": "bias+requant u8 (scale 2.0, zp 128)", "kernel": args.kernel,
                        "l2": "no flush: each step touches ~768 MB >> 126 MB L2",
-                       "parallelism": f"token-shard x{world} (no collective)",
+                       "parallelism": (f"row-shard x{world} + NCCL all-gather of the u8 outputs" if rows_mode
+                                       else f"token-shard x{world} (no collective)"),
                        "launch": "eager" if args.no_graphs else "CUDA graph per linear (replay)"},
             "gpu_launches": launches_per_step * args.steps,
             "per_linear": per_layer_info,
