@@ -190,3 +190,89 @@ extern "C" double tma_bw2(const void *buf, long rows_total, int S, int box_rows,
     cudaEventElapsedTime(&ms, a, b);
     return (double)ctas * iters * box_rows * 128.0 * boxes_per_stage * reps / (ms * 1e-3) / 1e9;
 }
+
+// ---- the pair kernel's exact TMA stream (BASELINE 5b geometry) without its
+// other roles: units (token tile nt, 256-row tile mt), m fastest, strided over
+// the pairs; per 128-k stage each CTA loads its W^T half box {128 m, 128 k}
+// and its X half box {128 tok, 128 k} (SWIZZLE_128B) onto the leader's barrier.
+__global__ void __cluster_dims__(2, 1, 1) tma_pairk_kernel(const __grid_constant__ CUtensorMap tw,
+                                                           const __grid_constant__ CUtensorMap tx, int S, int mtiles,
+                                                           int ntiles, int kchunks, int nprod, int mode)
+{
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
+    constexpr int SLOT = 32768;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * SLOT);
+    uint64_t *empty = full + S;
+    const uint32_t rank = tc::cluster_ctarank();
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+        tc::mbar_fence_init();
+    }
+    tc::cluster_sync();
+    const int w = threadIdx.x >> 5;
+    const int units = mtiles * ntiles;
+    const uint32_t full0 = tc::mapa(tc::smem_u32(full), 0);
+    if (w >= 2 && w < 2 + nprod) {
+        const int prod = w - 2;
+        int stage = 0, it = 0;
+        uint32_t phase = 0;
+        for (int u = pair; u < units; u += npairs) {
+            const int nt = u / mtiles, mt = u % mtiles;
+            for (int kc = 0; kc < kchunks; ++kc, ++it) {
+                if (it % nprod == prod) {
+                    tc::mbar_spin(&empty[stage], phase ^ 1);
+                    if (rank == 0) tcw::mbar_expect_tx(&full[stage], 2 * SLOT);
+                    uint8_t *a = smem + stage * SLOT;
+                    tcw::tma_load_2d_2sm(a, &tw, full0 + 8 * stage, mt * 256 + 128 * (int)rank, kc * 128);
+                    tcw::tma_load_2d_2sm(a + 16384, &tx, full0 + 8 * stage, nt * 256 + 128 * (int)rank, kc * 128);
+                }
+                if (++stage == S) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (w == 1 && rank == 0) {
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int u = pair; u < units; u += npairs)
+            for (int kc = 0; kc < kchunks; ++kc) {
+                tc::mbar_spin(&full[stage], phase);
+                tcw::mma_commit_2sm_mc(&empty[stage], 0x3);
+                if (++stage == S) { stage = 0; phase ^= 1; }
+            }
+    }
+    tc::cluster_sync();
+    (void)mode;
+}
+
+extern "C" double tma_pairk(const void *wt, const void *x, int M, int K, int N, int S, int nprod, int reps)
+{
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess) return -1;
+    auto enc = reinterpret_cast<EncodeTiledFn>(fn);
+    CUtensorMap tw, tx;
+    cuuint64_t dw[2] = {(cuuint64_t)M, (cuuint64_t)K}, sw[1] = {(cuuint64_t)M};
+    cuuint64_t dx[2] = {(cuuint64_t)N, (cuuint64_t)K}, sx[1] = {(cuuint64_t)N};
+    cuuint32_t box[2] = {128, 128}, es[2] = {1, 1};
+    if (enc(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(wt), dw, sw, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ||
+        enc(&tx, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(x), dx, sx, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE))
+        return -2;
+    const int smem = S * 32768 + 1024 + 1024;
+    if (cudaFuncSetAttribute(tma_pairk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return -3;
+    const int mtiles = M / 256, ntiles = N / 256, kchunks = K / 128;
+    tma_pairk_kernel<<<148, 64 + 32 * nprod, smem>>>(tw, tx, S, mtiles, ntiles, kchunks, nprod, 0);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    for (int r = 0; r < reps; ++r) tma_pairk_kernel<<<148, 64 + 32 * nprod, smem>>>(tw, tx, S, mtiles, ntiles, kchunks, nprod, 0);
+    cudaEventRecord(b);
+    if (cudaEventSynchronize(b) != cudaSuccess) return -4;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms * 1e3 / reps;   // us per sweep
+}
