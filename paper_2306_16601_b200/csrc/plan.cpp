@@ -672,8 +672,13 @@ static Layout make_layout(const si_weight *w, const si_program *p, const Compile
     const int64_t G = w->rows / 4, T = w->group_ptr[G], tiles = T / 4;
     const int64_t M = w->logical_rows;
     const int64_t mt = (M + 127) / 128, kp = (w->cols + 127) / 128 * 128;
-    uint64_t cur = align16(sizeof(SiImage));
-    auto put = [&](int i, uint64_t bytes) { l.off[i] = cur; cur = align16(cur + bytes); };
+    // every section starts on a 1024-byte boundary: the TMA boxes of the
+    // tensor-core operand sections read 128-byte rows, and a row straddling two
+    // L2 lines doubles the line requests (the W^T section used to sit at 16 or
+    // 80 mod 128)
+    auto align1k = [](uint64_t v) { return (v + 1023) & ~uint64_t(1023); };
+    uint64_t cur = align1k(sizeof(SiImage));
+    auto put = [&](int i, uint64_t bytes) { l.off[i] = cur; cur = align1k(cur + bytes); };
     put(0, 4 * (G + 1));
     put(1, 16 * tiles);
     put(2, 16 * tiles);

@@ -340,7 +340,7 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
                 int nt, m_lo, m_hi;
                 unit_range(unit, nt, m_lo, m_hi);
                 for (int mt = m_lo; mt < m_hi; ++mt) {
-                    tc::mbar_spin(&tempty[acc], acc_phase ^ 1);
+                    if (!(P.debug & 262144)) tc::mbar_spin(&tempty[acc], acc_phase ^ 1);   // experiment: no wait
                     tc::tc_fence_after();
                     const uint32_t d_tmem = tmem_base + acc * TILE_N;
                     for (int kc = 0; kc < P.kchunks; ++kc) {
@@ -388,6 +388,14 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
                 const uint32_t te = tempty0 + 8 * acc;
                 uint64_t *tf = &tfull[acc];
                 const uint32_t ph = acc_phase;
+                if (P.debug & 524288) {   // experiment: bare handshake (wait, release)
+                    tc::mbar_wait(tf, ph);
+                    __syncwarp();
+                    if (lane == 0) tc::mbar_arrive_cluster(te);
+                    acc ^= 1;
+                    if (acc == 0) acc_phase ^= 1;
+                    continue;
+                }
                 epi_tile<MODE, OUTK>(tmem_base, acc * TILE_N, mt * 256 + 128 * (int)rank, (int64_t)nt * TILE_N,
                                      &tmap_o, P, E, W, [tf, ph] { tc::mbar_wait(tf, ph); },
                                      [te] { tc::mbar_arrive_cluster(te); });

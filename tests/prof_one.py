@@ -24,10 +24,22 @@ for i in range(reps):
     out = K.spmm_exec(plan, act, out=out, kernel=kernel)
 torch.cuda.synchronize()
 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-s.record()
-for i in range(reps):
-    K.spmm_exec(plan, act, out=out, kernel=kernel)
-e.record()
+if os.environ.get("SI_PROF_GRAPH"):
+    # the reps replayed from one CUDA graph (no host launch cost between them)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(reps):
+            K.spmm_exec(plan, act, out=out, kernel=kernel)
+    g.replay()
+    torch.cuda.synchronize()
+    s.record()
+    g.replay()
+    e.record()
+else:
+    s.record()
+    for i in range(reps):
+        K.spmm_exec(plan, act, out=out, kernel=kernel)
+    e.record()
 torch.cuda.synchronize()
 ms = s.elapsed_time(e) / reps
 print(f"{name} kernel={kernel} {ms*1e3:.1f} us  {c.ops()/ms/1e9:.1f} TOPS  {c.hbm_bytes()/ms/1e6:.1f} GB/s")

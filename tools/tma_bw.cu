@@ -199,19 +199,27 @@ __global__ void __cluster_dims__(2, 1, 1) tma_pairk_kernel(const __grid_constant
                                                            const __grid_constant__ CUtensorMap tx, int S, int mtiles,
                                                            int ntiles, int kchunks, int nprod, int mode)
 {
+    // mode bits: 1 allocate 512 TMEM columns (pair), 2 sixteen extra warps
+    // parked on a barrier until the end (the kernel's epilogue warps)
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
     constexpr int SLOT = 32768;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * SLOT);
     uint64_t *empty = full + S;
+    uint64_t *done = empty + S;
+    uint32_t *tslot = reinterpret_cast<uint32_t *>(done + 1);
     const uint32_t rank = tc::cluster_ctarank();
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+        tc::mbar_init(done, 1);
         tc::mbar_fence_init();
     }
-    tc::cluster_sync();
     const int w = threadIdx.x >> 5;
+    if ((mode & 1) && w == 0) tc::tmem_alloc_2sm(tslot, 512);
+    tc::tc_fence_before();
+    tc::cluster_sync();
+    tc::tc_fence_after();
     const int units = mtiles * ntiles;
     const uint32_t full0 = tc::mapa(tc::smem_u32(full), 0);
     if (w >= 2 && w < 2 + nprod) {
@@ -240,12 +248,22 @@ __global__ void __cluster_dims__(2, 1, 1) tma_pairk_kernel(const __grid_constant
                 tcw::mma_commit_2sm_mc(&empty[stage], 0x3);
                 if (++stage == S) { stage = 0; phase ^= 1; }
             }
+        if ((threadIdx.x & 31) == 0) {
+            tc::mbar_arrive(done);
+            tc::mbar_arrive_cluster(tc::mapa(tc::smem_u32(done), 1));
+        }
+    } else if (w >= 2 + nprod && (mode & 2)) {
+        tc::mbar_wait(done, 0);
     }
+    tc::tc_fence_before();
     tc::cluster_sync();
-    (void)mode;
+    if ((mode & 1) && w == 0) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc_2sm(*tslot, 512);
+    }
 }
 
-extern "C" double tma_pairk(const void *wt, const void *x, int M, int K, int N, int S, int nprod, int reps)
+extern "C" double tma_pairk(const void *wt, const void *x, int M, int K, int N, int S, int nprod, int reps, int mode)
 {
     void *fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -264,12 +282,13 @@ extern "C" double tma_pairk(const void *wt, const void *x, int M, int K, int N, 
     if (cudaFuncSetAttribute(tma_pairk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
         return -3;
     const int mtiles = M / 256, ntiles = N / 256, kchunks = K / 128;
-    tma_pairk_kernel<<<148, 64 + 32 * nprod, smem>>>(tw, tx, S, mtiles, ntiles, kchunks, nprod, 0);
+    const int threads = 64 + 32 * nprod + ((mode & 2) ? 32 * 16 : 0);
+    tma_pairk_kernel<<<148, threads, smem>>>(tw, tx, S, mtiles, ntiles, kchunks, nprod, mode);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a);
-    for (int r = 0; r < reps; ++r) tma_pairk_kernel<<<148, 64 + 32 * nprod, smem>>>(tw, tx, S, mtiles, ntiles, kchunks, nprod, 0);
+    for (int r = 0; r < reps; ++r) tma_pairk_kernel<<<148, threads, smem>>>(tw, tx, S, mtiles, ntiles, kchunks, nprod, mode);
     cudaEventRecord(b);
     if (cudaEventSynchronize(b) != cudaSuccess) return -4;
     float ms = 0;

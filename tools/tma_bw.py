@@ -103,20 +103,20 @@ def pitch_sweep():
             print(f"pitch {pitch:6d} B, box {box} rows x 128 B, S {S}, 4 producers: {bw:6.1f} GB/s per SM", flush=True)
 
 
-def pairk():
+def pairk(S=4, nprod=3, mode=0):
     """The pair kernel's TMA stream for BASELINE 5b (W^T 1024x4096, X 1024x65536)
-    with no other roles: microseconds per sweep, vs the kernel's TMA-only run."""
+    with no other roles: microseconds per sweep, vs the kernel's TMA-only run.
+    mode bits: 1 TMEM allocated, 2 sixteen parked warps."""
     L = ctypes.CDLL(SO)
     L.tma_pairk.restype = ctypes.c_double
-    L.tma_pairk.argtypes = [ctypes.c_void_p, ctypes.c_void_p] + [ctypes.c_int] * 6
+    L.tma_pairk.argtypes = [ctypes.c_void_p, ctypes.c_void_p] + [ctypes.c_int] * 7
     M, K, N = 4096, 1024, 65536
     wt = torch.randint(0, 255, (K * M,), dtype=torch.uint8, device="cuda")
     x = torch.randint(0, 255, (K * N,), dtype=torch.uint8, device="cuda")
-    for S in (4, 6):
-        for nprod in (1, 3, 6):
-            us = L.tma_pairk(wt.data_ptr(), x.data_ptr(), M, K, N, S, nprod, 5)
-            gb = (K * N * (M // 256) + K * M * (N // 256)) / (us * 1e-6) / 1e9
-            print(f"5b pair TMA stream S {S} producers {nprod}: {us:7.1f} us  ({gb / 148:5.1f} GB/s per SM)", flush=True)
+    us = L.tma_pairk(wt.data_ptr(), x.data_ptr(), M, K, N, S, nprod, 5, mode)
+    gb = (K * N * (M // 256) + K * M * (N // 256)) / (us * 1e-6) / 1e9
+    print(f"5b pair TMA stream S {S} producers {nprod} mode {mode}: {us:7.1f} us  ({gb / 148:5.1f} GB/s per SM)",
+          flush=True)
 
 
 def latency_sweep():
@@ -148,7 +148,7 @@ if __name__ == "__main__":
         shared_sweep()
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "pairk":
-        pairk()
+        pairk(*[int(v) for v in sys.argv[2:5]])
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "pitch":
         pitch_sweep()
