@@ -106,7 +106,9 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
     const uint32_t tmem_base = *tmem_slot;
 
     const int prod = producer_index(warp, 2 + EPI_WARPS);
-    const int nprod = (P.debug & 4096) ? 1 : NPROD;   // 4096: single producer (A/B)
+    // (a producer must never run more than one ring round ahead of the
+    // slot it waits on: parity waits cannot tell rounds r-1 and r-3 apart)
+    const int nprod = (P.debug & 4096) ? 1 : (NPROD < STAGES ? NPROD : STAGES);   // 4096: single producer
     if (prod >= 0) {
         if (lane == 0) {
             int stage = 0, it = 0;
@@ -283,7 +285,9 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
     };
 
     const int prod = producer_index(warp, 2 + EPI_WARPS);
-    const int nprod = (P.debug & 4096) ? 1 : NPROD;   // 4096: single producer (A/B)
+    // (a producer must never run more than one ring round ahead of the
+    // slot it waits on: parity waits cannot tell rounds r-1 and r-3 apart)
+    const int nprod = (P.debug & 4096) ? 1 : (NPROD < STAGES ? NPROD : STAGES);   // 4096: single producer
     if (prod >= 0) {
         {   // whole warp, one elected lane issues (tcw::)
             // ---------------- TMA producers (both CTAs; bytes land on the leader's barriers)
@@ -488,7 +492,9 @@ k2m_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
     const uint32_t tmem_base = *tmem_slot;
 
     const int prod = producer_index(warp, 2 + EPI_WARPS);
-    const int nprod = (P.debug & 4096) ? 1 : NPROD;   // 4096: single producer (A/B)
+    // (a producer must never run more than one ring round ahead of the
+    // slot it waits on: parity waits cannot tell rounds r-1 and r-3 apart)
+    const int nprod = (P.debug & 4096) ? 1 : (NPROD < STAGES ? NPROD : STAGES);   // 4096: single producer
     if (prod >= 0) {
         {   // ---------------- TMA producers (whole warp, one elected lane issues)
             const uint32_t full_lead = tc::mapa(tc::smem_u32(full), lead);
@@ -930,7 +936,9 @@ k2s_kernel(const __grid_constant__ CUtensorMap tmap_s, const __grid_constant__ C
     const uint32_t tmem_base = *tmem_slot;
 
     const int prod = producer_index(warp, 2 + SP_EPI_WARPS);
-    const int nprod = (P.debug & 4096) ? 1 : NPROD;   // 4096: single producer (A/B)
+    // (a producer must never run more than one ring round ahead of the
+    // slot it waits on: parity waits cannot tell rounds r-1 and r-3 apart)
+    const int nprod = (P.debug & 4096) ? 1 : (NPROD < STAGES ? NPROD : STAGES);   // 4096: single producer
     if (prod >= 0) {
         if (lane == 0) {
             // ---------------- TMA producers (both CTAs; bytes land on the leader's barriers)
@@ -1215,7 +1223,10 @@ int k2_launch(const SpmmArgs &a)
     // measured default ("K2 variants"): the CTA pair unless the
     // weight has a single 128-row tile; the other variants stay selectable
     // (SI_K2_VARIANT) for tuning
-    int variant = forced >= 0 ? forced : (h->tc_mtiles <= 1 ? V_SINGLE : V_PAIR);
+    // [K, N] activations take the 256-k-stage pair (after the plan-image
+    // alignment fix it measures best on every config-5 linear: 52.4 / 177.5 /
+    // 167.9 us vs pair 54.5 / 197.0 / 169.4); token-major X the 128-k pair
+    int variant = forced >= 0 ? forced : h->tc_mtiles <= 1 ? V_SINGLE : a.layout == 0 ? V_PAIR256 : V_PAIR;
     if (variant == V_PAIR_XSTAT && h->tc_kpad > KMAX_XSTAT) variant = V_PAIR;
     if (variant == V_EXPAND_XSTAT && h->tc_kpad > KMAX_XSTAT) variant = V_EXPAND;
     if (variant == V_SPARSE && a.layout != 0) variant = V_PAIR;   // k2s reads X as [K, N]

@@ -18,7 +18,8 @@ if timeout 600 $CMD > gpurun_out/plain_launch.log 2>&1; then
 fi
 P1="python tests/prof_one.py c5b auto 3"
 if timeout 300 $P1 > gpurun_out/plain_prof.log 2>&1; then
-  timeout 900 ncu --set full --clock-control none -k regex:k2 -s 2 -c 1 \
+  rm -f /tmp/prof_top.ncu-rep
+  timeout 900 ncu -f --set full --clock-control none -k regex:k2 -s 2 -c 1 \
      -o /tmp/prof_top $P1 > gpurun_out/ncu_full.log 2>&1
   ncu -i /tmp/prof_top.ncu-rep --page raw --csv > gpurun_out/prof_top_raw.csv 2>/dev/null
   ncu -i /tmp/prof_top.ncu-rep --page details --csv > gpurun_out/prof_top_details.csv 2>/dev/null
