@@ -326,7 +326,10 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
                             if (P.b_mn_major)
                                 tcw::tma_load_2d_2sm(a_s + P_A, &tmap_x, fb, ltok, kc * BKS);
                             else
-                                tcw::tma_load_2d_2sm(a_s + P_A, &tmap_x, fb, kc * BKS, ltok);
+                                // token-major X: K-major boxes span at most 128 k (one
+                                // SWIZZLE_128B row), so a 256-k stage is two stacked tiles
+                                for (int h = 0; h < BKS / BK; ++h)
+                                    tcw::tma_load_2d_2sm(a_s + P_A + h * (128 * BK), &tmap_x, fb, kc * BKS + h * BK, ltok);
                         }
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
@@ -356,8 +359,9 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
 #pragma unroll
                         for (int kk = 0; kk < ((P.debug & 16) ? 0 : BKS / 32); ++kk) {
                             const uint64_t adesc = tc::smem_desc_sw128(a_addr + kk * 4096, P_A, 1024);
-                            const uint64_t bdesc = P.b_mn_major ? tc::smem_desc_sw128(b_addr + kk * 4096, P_B, 1024)
-                                                                : tc::smem_desc_sw128(b_addr + kk * 32, 16, 1024);
+                            const uint64_t bdesc =
+                                P.b_mn_major ? tc::smem_desc_sw128(b_addr + kk * 4096, P_B, 1024)
+                                             : tc::smem_desc_sw128(b_addr + (kk >> 2) * (128 * BK) + (kk & 3) * 32, 16, 1024);
                             tcw::mma_i8_2sm(d_tmem, adesc, bdesc, idesc, (kc | kk) ? 1u : 0u);
                         }
                         if (P.debug & 65536) {
@@ -1226,11 +1230,10 @@ int k2_launch(const SpmmArgs &a)
     // [K, N] activations take the 256-k-stage pair (after the plan-image
     // alignment fix it measures best on every config-5 linear: 52.4 / 177.5 /
     // 167.9 us vs pair 54.5 / 197.0 / 169.4); token-major X the 128-k pair
-    int variant = forced >= 0 ? forced : h->tc_mtiles <= 1 ? V_SINGLE : a.layout == 0 ? V_PAIR256 : V_PAIR;
+    int variant = forced >= 0 ? forced : h->tc_mtiles <= 1 ? V_SINGLE : V_PAIR256;
     if (variant == V_PAIR_XSTAT && h->tc_kpad > KMAX_XSTAT) variant = V_PAIR;
     if (variant == V_EXPAND_XSTAT && h->tc_kpad > KMAX_XSTAT) variant = V_EXPAND;
     if (variant == V_SPARSE && a.layout != 0) variant = V_PAIR;   // k2s reads X as [K, N]
-    if (variant == V_PAIR256 && a.layout != 0) variant = V_PAIR;  // 256-k boxes: [K, N] activations
     // X-sharing clusters: [K, N] activations and whole groups of XM pair tiles
     if ((variant == V_MC2 || variant == V_MC4) && a.layout != 0) variant = V_PAIR;
     if (variant == V_MC4 && ((h->tc_mtiles + 1) / 2) % 4) variant = V_MC2;
