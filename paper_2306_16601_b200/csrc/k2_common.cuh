@@ -416,17 +416,30 @@ __device__ __forceinline__ void epi_tile(uint32_t tmem_base, uint32_t tmem_col, 
         }
         if (acc == 0x12345678u && m == -1) reinterpret_cast<uint32_t *>(P.out)[0] = acc;
     } else if (!(P.debug & 1)) {
+        // the accumulator is released as soon as the last chunk is in
+        // registers (before its math and staging), so the MMAs of the tile
+        // after next can start that much earlier
+        auto rel = [&]() {
+            tc::tc_fence_before();
+            __syncwarp();
+            if (W.lane == 0) release();
+        };
 #pragma unroll 1
         for (int c = 0; c < COLS / 32; ++c) {
             const int col = W.g * COLS + c * 32;
-            epi_chunk<MODE, OUTK, RES>(tmem_base + ((uint32_t)(W.q * 32) << 16) + tmem_col + col, m, mok, adj, s_in,
-                                       cq, gm, fast, tok0 + col, c, P, E, W, rp0, rp1);
+            const uint32_t ta = tmem_base + ((uint32_t)(W.q * 32) << 16) + tmem_col + col;
+            if (c == COLS / 32 - 1)
+                epi_chunk<MODE, OUTK, RES>(ta, m, mok, adj, s_in, cq, gm, fast, tok0 + col, c, P, E, W, rp0, rp1, rel);
+            else
+                epi_chunk<MODE, OUTK, RES>(ta, m, mok, adj, s_in, cq, gm, fast, tok0 + col, c, P, E, W, rp0, rp1);
         }
     }
-    // this warp's TMEM reads are complete: release the accumulator
-    tc::tc_fence_before();
-    __syncwarp();
-    if (W.lane == 0) release();
+    if (P.debug & (1 | 16384)) {
+        // (experiments) this warp's TMEM reads are complete: release the accumulator
+        tc::tc_fence_before();
+        __syncwarp();
+        if (W.lane == 0) release();
+    }
     if constexpr (STAGED) {
         tc::fence_proxy_async_smem();
         tc::named_bar_sync(1 + W.g, 128);
