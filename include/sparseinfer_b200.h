@@ -197,6 +197,15 @@ int32_t si_bmm_f32(const float *a, const float *b, float *out, int64_t nb0, int6
 int32_t si_quantize_f32(const float *x, int64_t n, float scale, int32_t zp, int32_t lo, int32_t hi, void *out,
                         void *stream);
 
+/* the encoder's attention block for one (sequence, head) per CTA, all in
+ * shared memory: scores = q k^T * alpha (bmm_nt), softmax_rows, context =
+ * p v (bmm_nn) -- eltwise.py:34-160 in those orders, so bit-equal to the three
+ * ops run separately.  qkv is token-major [batch*seq, ld_qkv] with q, k, v at
+ * columns 0, H, 2H (H = heads*head_dim); ctx is [batch*seq, ld_ctx].
+ * SI_EUNSUPPORTED for seq > 128 or head_dim > 64 (use the separate ops). */
+int32_t si_attention_f32(const float *qkv, float *ctx, int64_t batch, int64_t seq, int64_t heads,
+                         int64_t head_dim, int64_t ld_qkv, int64_t ld_ctx, float alpha, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

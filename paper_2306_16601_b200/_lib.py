@@ -74,11 +74,12 @@ def lib():
     L.si_layer_norm_f32.argtypes = [_vp, _vp, _vp, ctypes.c_double, _vp, _i64, _i64, _vp]
     L.si_bmm_f32.argtypes = [_vp, _vp, _vp] + [_i64] * 14 + [_i32, ctypes.c_float, _vp]
     L.si_quantize_f32.argtypes = [_vp, _i64, ctypes.c_float, _i32, _i32, _i32, _vp, _vp]
+    L.si_attention_f32.argtypes = [_vp, _vp] + [_i64] * 6 + [ctypes.c_float, _vp]
     for f in ("si_plan_image_size", "si_plan_image_build", "si_plan_info_get",
               "si_spmm_workspace_size", "si_spmm_launch_count", "si_spmm",
               "si_spmm_host_workspace_size", "si_spmm_host",
               "si_spmm_host_batch_workspace_size", "si_spmm_host_batch",
-              "si_softmax_rows_f32", "si_layer_norm_f32", "si_bmm_f32", "si_quantize_f32"):
+              "si_softmax_rows_f32", "si_layer_norm_f32", "si_bmm_f32", "si_quantize_f32", "si_attention_f32"):
         getattr(L, f).restype = _i32
     if L.si_abi_version() != 1:
         raise RuntimeError("libsparseinfer_b200 ABI version mismatch")

@@ -240,7 +240,7 @@ inline bool rows_fit(int64_t n) { return n <= 4096 && (int64_t)ROWS * (n + 1) * 
 // output tiles, 256 threads with 4x4 register blocks; A and B panels staged
 // in shared memory 16 k at a time, coalesced along each operand's contiguous
 // dimension.
-constexpr int BT = 64, BK = 16;
+constexpr int BT = 64, BK = 32;
 __global__ void __launch_bounds__(256) k_bmm(const float *a, const float *b, float *out, int64_t nb1, int64_t m,
                                              int64_t k, int64_t n, int64_t sa0, int64_t sa1, int64_t lda, int64_t sb0,
                                              int64_t sb1, int64_t ldb, int64_t so0, int64_t so1, int64_t ldo,
@@ -389,6 +389,191 @@ extern "C" int32_t si_quantize_f32(const float *x, int64_t n, float scale, int32
     const int threads = 256;
     const int64_t blocks = imin64((n + threads - 1) / threads, 148 * 16);
     k_quantize<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(x, n, (double)scale, zp, lo, hi, out, lo < 0);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { si_set_error(cudaGetErrorString(e)); return SI_ECUDA; }
+    return SI_OK;
+}
+
+// ---- fused attention block of the encoder: per (sequence, head), scores,
+// softmax and context in one CTA with everything in shared memory.  The same
+// three reference operators in the same orders (bmm_nt * alpha, softmax_rows,
+// bmm_nn; eltwise.py:34-160), so the result equals the unfused ops bit for
+// bit, without the scores' round trip through HBM.
+namespace {
+constexpr int AT_S = 128, AT_D = 64;   // supported maximum seq, head dim
+constexpr int AT_LP = AT_S + 1;        // row stride of the probabilities
+// smem: [ Qt | Kt ] (transposed, [D][S] each) aliased by P [S][S+1] once the
+// scores are in registers, then V [S][D]: ~98 KB, two CTAs per SM.
+constexpr int AT_QK = 2 * AT_D * AT_S > AT_S * AT_LP ? 2 * AT_D * AT_S : AT_S * AT_LP;
+constexpr int AT_SMEM = (AT_QK + AT_S * AT_D) * 4;
+
+__global__ void __launch_bounds__(256, 2) k_attention(const float *qkv, float *ctx, int64_t seq, int64_t heads,
+                                                      int64_t d, int64_t ld, int64_t ldo, float alpha)
+{
+    extern __shared__ __align__(16) float sm[];
+    float *Qt = sm;                    // [D][S]
+    float *Kt = sm + AT_D * AT_S;      // [D][S]
+    float *Ps = sm;                    // [S][S+1], after the scores
+    float *Vs = sm + AT_QK;            // [S][D]
+    const int64_t b = blockIdx.x / heads, h = blockIdx.x % heads;
+    const int t = threadIdx.x;
+    const int S = (int)seq, D = (int)d;
+    const float *base = qkv + b * seq * ld + h * d;
+    const int64_t H = heads * d;
+    if (((D | ld | H | h * d) & 3) == 0 && (reinterpret_cast<uintptr_t>(qkv) & 15) == 0) {
+        // 16-byte loads, all of a thread's loads in flight before the stores
+        const int D4 = D >> 2, n4 = S * D4;
+        for (int e0 = t; e0 < n4; e0 += 256 * 4) {
+            float4 q[4], k[4], v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * 256;
+                if (e < n4) {
+                    const int i = e / D4, p4 = e - i * D4;
+                    const float4 *row = reinterpret_cast<const float4 *>(base + i * ld) + p4;
+                    q[u] = __ldg(row);
+                    k[u] = __ldg(row + H / 4);
+                    v[u] = __ldg(row + H / 2);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * 256;
+                if (e < n4) {
+                    const int i = e / D4, p = (e - i * D4) * 4;
+                    Qt[(p + 0) * AT_S + i] = q[u].x; Qt[(p + 1) * AT_S + i] = q[u].y;
+                    Qt[(p + 2) * AT_S + i] = q[u].z; Qt[(p + 3) * AT_S + i] = q[u].w;
+                    Kt[(p + 0) * AT_S + i] = k[u].x; Kt[(p + 1) * AT_S + i] = k[u].y;
+                    Kt[(p + 2) * AT_S + i] = k[u].z; Kt[(p + 3) * AT_S + i] = k[u].w;
+                    *reinterpret_cast<float4 *>(Vs + i * AT_D + p) = v[u];
+                }
+            }
+        }
+    } else {
+        for (int e = t; e < S * D; e += 256) {
+            const int i = e / D, p = e - i * D;
+            const float *row = base + i * ld;
+            Qt[p * AT_S + i] = row[p];
+            Kt[p * AT_S + i] = row[H + p];
+            Vs[i * AT_D + p] = row[2 * H + p];
+        }
+    }
+    __syncthreads();
+    // scores: a 4 x 16 block per thread (rows 4*ib.., columns 16*jb..); every
+    // output still sums p = 0..D-1 in order with separate mul and add
+    const int jb = t & 7, ib = t >> 3;
+    {
+        float acc[4][16];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 16; ++c) acc[r][c] = 0.0f;
+        for (int p = 0; p < D; ++p) {
+            const float4 q = *reinterpret_cast<const float4 *>(Qt + p * AT_S + ib * 4);
+            float kv[16];
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+                const float4 k4 = *reinterpret_cast<const float4 *>(Kt + p * AT_S + jb * 16 + c4 * 4);
+                kv[c4 * 4 + 0] = k4.x; kv[c4 * 4 + 1] = k4.y; kv[c4 * 4 + 2] = k4.z; kv[c4 * 4 + 3] = k4.w;
+            }
+            const float qv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int c = 0; c < 16; ++c) acc[r][c] = __fadd_rn(acc[r][c], __fmul_rn(qv[r], kv[c]));
+        }
+        __syncthreads();   // Qt / Kt dead: P takes their place
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int i = ib * 4 + r;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                const int j = jb * 16 + c;
+                if (i < S && j < S) Ps[i * AT_LP + j] = __fmul_rn(acc[r][c], alpha);
+            }
+        }
+    }
+    __syncthreads();
+    // softmax in the reference's order: the row max and the f64 sum stay
+    // sequential per row; the exps and the final scaling are elementwise
+    __shared__ float rmax[AT_S], rinv[AT_S];
+    if (t < S) {
+        const float *r = Ps + t * AT_LP;
+        float m = r[0];
+        for (int c = 1; c < S; ++c)
+            if (r[c] > m) m = r[c];
+        rmax[t] = m;
+    }
+    __syncthreads();
+    for (int e = t; e < S * S; e += 256) {
+        const int i = e / S, c = e - i * S;
+        Ps[i * AT_LP + c] = (float)exp((double)Ps[i * AT_LP + c] - (double)rmax[i]);
+    }
+    __syncthreads();
+    if (t < S) {
+        const float *r = Ps + t * AT_LP;
+        double s = 0.0;
+        for (int c = 0; c < S; ++c) s = __dadd_rn(s, (double)r[c]);
+        rinv[t] = (float)(1.0 / s);
+    }
+    __syncthreads();
+    for (int e = t; e < S * S; e += 256) {
+        const int i = e / S, c = e - i * S;
+        Ps[i * AT_LP + c] = __fmul_rn(Ps[i * AT_LP + c], rinv[i]);
+    }
+    __syncthreads();
+    // context: a 4 x 8 block per thread, p = 0..S-1 in order
+    {
+        float acc[4][8];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[r][c] = 0.0f;
+        for (int p = 0; p < S; ++p) {
+            float pv[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) pv[r] = Ps[min(ib * 4 + r, AT_S - 1) * AT_LP + p];
+            const float4 v0 = *reinterpret_cast<const float4 *>(Vs + p * AT_D + jb * 8);
+            const float4 v1 = *reinterpret_cast<const float4 *>(Vs + p * AT_D + jb * 8 + 4);
+            const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) acc[r][c] = __fadd_rn(acc[r][c], __fmul_rn(pv[r], vv[c]));
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int i = ib * 4 + r;
+            if (i >= S) continue;
+            float *o = ctx + (b * seq + i) * ldo + h * d;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                if (jb * 8 + c < D) o[jb * 8 + c] = __fmul_rn(acc[r][c], 1.0f);
+        }
+    }
+}
+}  // namespace
+
+extern "C" int32_t si_attention_f32(const float *qkv, float *ctx, int64_t batch, int64_t seq, int64_t heads,
+                                    int64_t head_dim, int64_t ld_qkv, int64_t ld_ctx, float alpha, void *stream)
+{
+    if (!qkv || !ctx || batch < 0 || seq <= 0 || heads <= 0 || head_dim <= 0) {
+        si_set_error("attention: bad arguments");
+        return SI_EINVAL;
+    }
+    if (seq > AT_S || head_dim > AT_D || head_dim > 64) {
+        si_set_error("attention: fused kernel supports seq <= 128 and head_dim <= 64");
+        return SI_EUNSUPPORTED;
+    }
+    if (batch == 0) return SI_OK;
+    const int smem = AT_SMEM;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    k_attention<<<(unsigned)(batch * heads), 256, smem, (cudaStream_t)stream>>>(qkv, ctx, seq, heads, head_dim, ld_qkv,
+                                                                               ld_ctx, alpha);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { si_set_error(cudaGetErrorString(e)); return SI_ECUDA; }
     return SI_OK;

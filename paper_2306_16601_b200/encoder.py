@@ -37,7 +37,7 @@ import numpy as np
 import torch
 
 from .kernels import build_program, plan_spmm, relayout_tokens, spmm_exec
-from .kernels.eltwise import attention_scale, bmm_strided, layer_norm_f32, quantize_f32, softmax_f32
+from .kernels.eltwise import attention_fused, attention_scale, bmm_strided, layer_norm_f32, quantize_f32, softmax_f32
 from .sparse import encode_sparse, generate_pattern_weight
 from .tensor import DType, QuantParams, u8_params_from_range
 
@@ -147,10 +147,11 @@ class BertEncoder:
     runs the whole stack with every linear on the sparse SpMM kernels."""
 
     def __init__(self, cfg: EncoderConfig = EncoderConfig(), device="cuda", kernel: str = "auto",
-                 weights: list | None = None):
+                 weights: list | None = None, fused_attention: bool = True):
         self.cfg = cfg
         self.device = torch.device(device)
         self.kernel = kernel
+        self.fused_attention = fused_attention   # si_attention_f32; False = the three separate ops
         self.layers = []
         for li in range(cfg.layers):
             lw = weights[li] if weights is not None else make_layer_weights(cfg, li)
@@ -181,12 +182,14 @@ class BertEncoder:
         B, S, H, nh = cfg.batch, cfg.seq, cfg.hidden, cfg.heads
         d = H // nh
         ld = 3 * H
+        ctx = torch.empty((B * S, H), dtype=torch.float32, device=qkv.device)
+        if self.fused_attention and attention_fused(qkv, ctx, B, S, nh, d, attention_scale(d)):
+            return ctx
         scores = torch.empty((B, nh, S, S), dtype=torch.float32, device=qkv.device)
         # scores[b, h] = q[b, :, h] @ k[b, :, h]^T * 1/sqrt(d); q at column h*d, k at H + h*d
         bmm_strided(qkv, qkv[:, H:], scores, B, nh, S, d, S, (S * ld, d, ld), (S * ld, d, ld),
                     (nh * S * S, S * S, S), True, attention_scale(d))
         softmax_f32(scores, out=scores)
-        ctx = torch.empty((B * S, H), dtype=torch.float32, device=qkv.device)
         bmm_strided(scores, qkv[:, 2 * H:], ctx, B, nh, S, S, d, (nh * S * S, S * S, S), (S * ld, d, ld),
                     (S * H, d, H), False, 1.0)
         return ctx

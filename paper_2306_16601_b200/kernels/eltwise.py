@@ -110,6 +110,20 @@ def quantize_f32(x: torch.Tensor, q: QuantParams, out: torch.Tensor | None = Non
     return out
 
 
+def attention_fused(qkv: torch.Tensor, ctx: torch.Tensor, batch: int, seq: int, heads: int, head_dim: int,
+                    alpha: float) -> bool:
+    """scores -> softmax -> context for every (sequence, head) in one kernel
+    (si_attention_f32), bit-equal to bmm_strided(nt) + softmax_f32 +
+    bmm_strided(nn).  Returns False (nothing launched) when the shape is
+    outside the fused kernel's smem budget (seq > 128 or head_dim > 64)."""
+    rc = _lib.lib().si_attention_f32(qkv.data_ptr(), ctx.data_ptr(), batch, seq, heads, head_dim, qkv.stride(0),
+                                     ctx.stride(0), float(np.float32(alpha)), _stream(qkv))
+    if rc == _lib.SI_EUNSUPPORTED:
+        return False
+    _lib.check(rc, "attention")
+    return True
+
+
 def attention_scale(head_dim: int) -> np.float32:
     """1/sqrt(d) as the f32 alpha of the scores product."""
     return np.float32(1.0 / math.sqrt(float(head_dim)))

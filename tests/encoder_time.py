@@ -59,6 +59,7 @@ def main():
     ctx = torch.empty((B * S, H), dtype=torch.float32, device="cuda")
     E.bmm_strided(scores, qkv[:, 2 * H:], ctx, B, nh, S, S, d, (nh * S * S, S * S, S), (S * ld, d, ld),
                   (S * H, d, H), False, 1.0); mark("  context bmm (NN)")
+    E.attention_fused(qkv, ctx, B, S, nh, d, E.attention_scale(d)); mark("  attention fused (same result)")
     cq = E.quantize_f32(ctx, q.qp_ctx); mark("quantize ctx")
     a = spmm_exec(L.plans["o"], relayout_tokens(cq), sides=x.view(1, cfg.tokens, cfg.hidden)); mark("spmm o +res")
     h1 = E.layer_norm_f32(a, L.gamma1, L.beta1, cfg.eps); mark("layer norm 1")

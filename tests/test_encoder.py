@@ -217,3 +217,39 @@ def test_gpu_bert_base_stack_config4():
     # LayerNorm output: per-row mean of (y - beta)/gamma ~ 0
     z = (y1 - L.beta2) / L.gamma2
     assert float(z.mean(dim=1).abs().max()) < 1e-3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("batch,seq,heads,d,pad", [(2, 128, 12, 64, 0), (2, 128, 12, 64, 5), (3, 77, 3, 48, 4),
+                                                   (1, 1, 2, 8, 0), (4, 128, 2, 33, 5), (2, 5, 1, 64, 4)])
+def test_gpu_fused_attention_equals_separate_ops(batch, seq, heads, d, pad):
+    """si_attention_f32 (scores, softmax and context in one CTA per
+    (sequence, head)) against the three separate ops: bit-equal, including
+    ragged seq / head_dim and qkv / ctx row strides wider than the data
+    (16-byte-aligned strides take the vector load path, the rest the scalar)."""
+    import torch
+    from paper_2306_16601_b200.kernels import eltwise as E
+    H = heads * d
+    rng = np.random.default_rng(seq * 7 + d)
+    qkv = _cuda(rng.normal(0, 2, (batch * seq, 3 * H + pad)).astype(np.float32))
+    alpha = E.attention_scale(d)
+    fused = torch.zeros((batch * seq, H + 3), dtype=torch.float32, device="cuda")
+    assert E.attention_fused(qkv, fused, batch, seq, heads, d, alpha)
+    ld = qkv.stride(0)
+    scores = torch.empty((batch, heads, seq, seq), dtype=torch.float32, device="cuda")
+    E.bmm_strided(qkv, qkv[:, H:], scores, batch, heads, seq, d, seq, (seq * ld, d, ld), (seq * ld, d, ld),
+                  (heads * seq * seq, seq * seq, seq), True, alpha)
+    E.softmax_f32(scores, out=scores)
+    ctx = torch.zeros((batch * seq, H + 3), dtype=torch.float32, device="cuda")
+    E.bmm_strided(scores, qkv[:, 2 * H:], ctx, batch, heads, seq, seq, d, (heads * seq * seq, seq * seq, seq),
+                  (seq * ld, d, ld), (seq * (H + 3), d, H + 3), False, 1.0)
+    assert torch.equal(fused, ctx)
+
+
+@pytest.mark.gpu
+def test_gpu_fused_attention_unsupported_shape():
+    import torch
+    from paper_2306_16601_b200.kernels import eltwise as E
+    qkv = torch.zeros((129, 3 * 64), dtype=torch.float32, device="cuda")
+    ctx = torch.zeros((129, 64), dtype=torch.float32, device="cuda")
+    assert not E.attention_fused(qkv, ctx, 1, 129, 1, 64, 0.125)
