@@ -401,18 +401,21 @@ extern "C" int32_t si_quantize_f32(const float *x, int64_t n, float scale, int32
 // bit, without the scores' round trip through HBM.
 namespace {
 constexpr int AT_S = 128, AT_D = 64;   // supported maximum seq, head dim
+constexpr int AT_LQ = AT_D + 4;        // q / k row stride: 16-byte rows, rows 4 banks apart
 constexpr int AT_LP = AT_S + 1;        // row stride of the probabilities
-// smem: [ Qt | Kt ] (transposed, [D][S] each) aliased by P [S][S+1] once the
-// scores are in registers, then V [S][D]: ~98 KB, two CTAs per SM.
-constexpr int AT_QK = 2 * AT_D * AT_S > AT_S * AT_LP ? 2 * AT_D * AT_S : AT_S * AT_LP;
+// smem: [ Q | K ] ([S][D+4] each) aliased by P [S][S+1] once the scores are
+// in registers, then V [S][D]: ~100 KB, two CTAs per SM.
+constexpr int AT_QK = 2 * AT_S * AT_LQ > AT_S * AT_LP ? 2 * AT_S * AT_LQ : AT_S * AT_LP;
 constexpr int AT_SMEM = (AT_QK + AT_S * AT_D) * 4;
 
+// two CTAs per SM (128 registers, a few spills) measured 248 us on config 4
+// against 268 us for one CTA per SM at 138 registers
 __global__ void __launch_bounds__(256, 2) k_attention(const float *qkv, float *ctx, int64_t seq, int64_t heads,
                                                       int64_t d, int64_t ld, int64_t ldo, float alpha)
 {
     extern __shared__ __align__(16) float sm[];
-    float *Qt = sm;                    // [D][S]
-    float *Kt = sm + AT_D * AT_S;      // [D][S]
+    float *Qs = sm;                    // [S][D+4]
+    float *Ks = sm + AT_S * AT_LQ;     // [S][D+4]
     float *Ps = sm;                    // [S][S+1], after the scores
     float *Vs = sm + AT_QK;            // [S][D]
     const int64_t b = blockIdx.x / heads, h = blockIdx.x % heads;
@@ -420,7 +423,8 @@ __global__ void __launch_bounds__(256, 2) k_attention(const float *qkv, float *c
     const int S = (int)seq, D = (int)d;
     const float *base = qkv + b * seq * ld + h * d;
     const int64_t H = heads * d;
-    if (((D | ld | H | h * d) & 3) == 0 && (reinterpret_cast<uintptr_t>(qkv) & 15) == 0) {
+    const bool vec = ((D | ld | H | h * d) & 3) == 0 && (reinterpret_cast<uintptr_t>(qkv) & 15) == 0;
+    if (vec) {
         // 16-byte loads, all of a thread's loads in flight before the stores
         const int D4 = D >> 2, n4 = S * D4;
         for (int e0 = t; e0 < n4; e0 += 256 * 4) {
@@ -441,10 +445,8 @@ __global__ void __launch_bounds__(256, 2) k_attention(const float *qkv, float *c
                 const int e = e0 + u * 256;
                 if (e < n4) {
                     const int i = e / D4, p = (e - i * D4) * 4;
-                    Qt[(p + 0) * AT_S + i] = q[u].x; Qt[(p + 1) * AT_S + i] = q[u].y;
-                    Qt[(p + 2) * AT_S + i] = q[u].z; Qt[(p + 3) * AT_S + i] = q[u].w;
-                    Kt[(p + 0) * AT_S + i] = k[u].x; Kt[(p + 1) * AT_S + i] = k[u].y;
-                    Kt[(p + 2) * AT_S + i] = k[u].z; Kt[(p + 3) * AT_S + i] = k[u].w;
+                    *reinterpret_cast<float4 *>(Qs + i * AT_LQ + p) = q[u];
+                    *reinterpret_cast<float4 *>(Ks + i * AT_LQ + p) = k[u];
                     *reinterpret_cast<float4 *>(Vs + i * AT_D + p) = v[u];
                 }
             }
@@ -453,14 +455,14 @@ __global__ void __launch_bounds__(256, 2) k_attention(const float *qkv, float *c
         for (int e = t; e < S * D; e += 256) {
             const int i = e / D, p = e - i * D;
             const float *row = base + i * ld;
-            Qt[p * AT_S + i] = row[p];
-            Kt[p * AT_S + i] = row[H + p];
+            Qs[i * AT_LQ + p] = row[p];
+            Ks[i * AT_LQ + p] = row[H + p];
             Vs[i * AT_D + p] = row[2 * H + p];
         }
     }
     __syncthreads();
-    // scores: a 4 x 16 block per thread (rows 4*ib.., columns 16*jb..); every
-    // output still sums p = 0..D-1 in order with separate mul and add
+    // scores: rows 4*ib + r, columns jb + 8*c; every output still sums
+    // p = 0..D-1 in order with separate mul and add
     const int jb = t & 7, ib = t >> 3;
     {
         float acc[4][16];
@@ -468,27 +470,42 @@ __global__ void __launch_bounds__(256, 2) k_attention(const float *qkv, float *c
         for (int r = 0; r < 4; ++r)
 #pragma unroll
             for (int c = 0; c < 16; ++c) acc[r][c] = 0.0f;
-        for (int p = 0; p < D; ++p) {
-            const float4 q = *reinterpret_cast<const float4 *>(Qt + p * AT_S + ib * 4);
-            float kv[16];
+        const int D4 = D & ~3;
+#pragma unroll 1
+        for (int p = 0; p < D4; p += 4) {
+            float4 q[4];
 #pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) {
-                const float4 k4 = *reinterpret_cast<const float4 *>(Kt + p * AT_S + jb * 16 + c4 * 4);
-                kv[c4 * 4 + 0] = k4.x; kv[c4 * 4 + 1] = k4.y; kv[c4 * 4 + 2] = k4.z; kv[c4 * 4 + 3] = k4.w;
+            for (int r = 0; r < 4; ++r) q[r] = *reinterpret_cast<const float4 *>(Qs + (ib * 4 + r) * AT_LQ + p);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                const float4 k = *reinterpret_cast<const float4 *>(Ks + (jb + 8 * c) * AT_LQ + p);
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    float a = acc[r][c];
+                    a = __fadd_rn(a, __fmul_rn(q[r].x, k.x));
+                    a = __fadd_rn(a, __fmul_rn(q[r].y, k.y));
+                    a = __fadd_rn(a, __fmul_rn(q[r].z, k.z));
+                    acc[r][c] = __fadd_rn(a, __fmul_rn(q[r].w, k.w));
+                }
             }
-            const float qv[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-#pragma unroll
-                for (int c = 0; c < 16; ++c) acc[r][c] = __fadd_rn(acc[r][c], __fmul_rn(qv[r], kv[c]));
         }
-        __syncthreads();   // Qt / Kt dead: P takes their place
+#pragma unroll 1
+        for (int p = D4; p < D; ++p) {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                const float k = Ks[(jb + 8 * c) * AT_LQ + p];
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    acc[r][c] = __fadd_rn(acc[r][c], __fmul_rn(Qs[(ib * 4 + r) * AT_LQ + p], k));
+            }
+        }
+        __syncthreads();   // Q / K dead: P takes their place
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             const int i = ib * 4 + r;
 #pragma unroll
             for (int c = 0; c < 16; ++c) {
-                const int j = jb * 16 + c;
+                const int j = jb + 8 * c;
                 if (i < S && j < S) Ps[i * AT_LP + j] = __fmul_rn(acc[r][c], alpha);
             }
         }
@@ -522,7 +539,8 @@ __global__ void __launch_bounds__(256, 2) k_attention(const float *qkv, float *c
         Ps[i * AT_LP + c] = __fmul_rn(Ps[i * AT_LP + c], rinv[i]);
     }
     __syncthreads();
-    // context: a 4 x 8 block per thread, p = 0..S-1 in order
+    // context: rows 4*ib + r, columns 4*jb + {0..3} and 32 + 4*jb + {0..3};
+    // p = 0..S-1 in order
     {
         float acc[4][8];
 #pragma unroll
@@ -533,8 +551,8 @@ __global__ void __launch_bounds__(256, 2) k_attention(const float *qkv, float *c
             float pv[4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) pv[r] = Ps[min(ib * 4 + r, AT_S - 1) * AT_LP + p];
-            const float4 v0 = *reinterpret_cast<const float4 *>(Vs + p * AT_D + jb * 8);
-            const float4 v1 = *reinterpret_cast<const float4 *>(Vs + p * AT_D + jb * 8 + 4);
+            const float4 v0 = *reinterpret_cast<const float4 *>(Vs + p * AT_D + jb * 4);
+            const float4 v1 = *reinterpret_cast<const float4 *>(Vs + p * AT_D + 32 + jb * 4);
             const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
             for (int r = 0; r < 4; ++r)
@@ -547,8 +565,10 @@ __global__ void __launch_bounds__(256, 2) k_attention(const float *qkv, float *c
             if (i >= S) continue;
             float *o = ctx + (b * seq + i) * ldo + h * d;
 #pragma unroll
-            for (int c = 0; c < 8; ++c)
-                if (jb * 8 + c < D) o[jb * 8 + c] = __fmul_rn(acc[r][c], 1.0f);
+            for (int c = 0; c < 8; ++c) {
+                const int j = (c < 4 ? 0 : 32) + jb * 4 + (c & 3);
+                if (j < D) o[j] = __fmul_rn(acc[r][c], 1.0f);
+            }
         }
     }
 }
