@@ -14,6 +14,7 @@
 
 #include "../../include/sparseinfer_b200.h"
 #include "si_internal.h"
+#include "tc_ptx.cuh"
 
 namespace {
 
@@ -231,6 +232,70 @@ __global__ void k_layer_norm_rows_smem(const float *x, const float *gamma, const
     store_rows(out, n, rows, r0, n, t_sm);
 }
 
+// The same computation for n % 4 == 0 with the 32 rows moved by the bulk-copy
+// engine: each lane issues the 1-D copy of its own row into a 16-byte-aligned
+// smem row (stride n + 4, so the lanes' float4 reads of a quarter warp hit
+// distinct banks), then streams its row back out the same way.  All of an
+// SM's rows are in flight at once instead of one warp's loads at a time.
+__global__ void k_layer_norm_rows_bulk(const float *x, const float *gamma, const float *beta, double eps, float *out,
+                                       int64_t rows, int n)
+{
+    extern __shared__ __align__(16) float b_sm[];
+    __shared__ __align__(8) uint64_t bar;
+    const int lane = threadIdx.x & 31;
+    const int64_t r0 = (int64_t)blockIdx.x * ROWS;
+    const int nr = (int)imin64(ROWS, rows - r0);
+    const int ldr = n + 4;
+    const uint32_t row_bytes = (uint32_t)n * 4;
+    if (lane == 0) {
+        tc::mbar_init(&bar, 1);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tc::mbar_expect_tx(&bar, row_bytes * (uint32_t)nr);
+    }
+    __syncwarp();
+    float *t = b_sm + lane * ldr;
+    if (lane < nr) tc::bulk_load(t, x + (r0 + lane) * n, row_bytes, &bar);
+    tc::mbar_wait(&bar, 0);
+    if (lane < nr) {
+        const float4 *t4 = reinterpret_cast<const float4 *>(t);
+        double s = 0.0;
+        for (int c = 0; c < n / 4; ++c) {
+            const float4 v = t4[c];
+            s = __dadd_rn(s, (double)v.x); s = __dadd_rn(s, (double)v.y);
+            s = __dadd_rn(s, (double)v.z); s = __dadd_rn(s, (double)v.w);
+        }
+        const double mean = __ddiv_rn(s, (double)n);
+        double v2 = 0.0;
+        for (int c = 0; c < n / 4; ++c) {
+            const float4 v = t4[c];
+            double d;
+            d = __dsub_rn((double)v.x, mean); v2 = __dadd_rn(v2, __dmul_rn(d, d));
+            d = __dsub_rn((double)v.y, mean); v2 = __dadd_rn(v2, __dmul_rn(d, d));
+            d = __dsub_rn((double)v.z, mean); v2 = __dadd_rn(v2, __dmul_rn(d, d));
+            d = __dsub_rn((double)v.w, mean); v2 = __dadd_rn(v2, __dmul_rn(d, d));
+        }
+        const float inv = (float)__ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__ddiv_rn(v2, (double)n), eps)));
+        const float mean32 = (float)mean;
+        float4 *w4 = reinterpret_cast<float4 *>(t);
+        const float4 *g4 = reinterpret_cast<const float4 *>(gamma), *b4 = reinterpret_cast<const float4 *>(beta);
+        for (int c = 0; c < n / 4; ++c) {
+            float4 v = w4[c];
+            const float4 g = __ldg(g4 + c), b = __ldg(b4 + c);
+            v.x = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(v.x, mean32), inv), g.x), b.x);
+            v.y = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(v.y, mean32), inv), g.y), b.y);
+            v.z = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(v.z, mean32), inv), g.z), b.z);
+            v.w = __fadd_rn(__fmul_rn(__fmul_rn(__fsub_rn(v.w, mean32), inv), g.w), b.w);
+            w4[c] = v;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + (r0 + lane) * n),
+                     "r"(tc::smem_u32(t)), "r"(row_bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+}
+
 constexpr int SMEM_ROWS_MAX = 200 * 1024;
 inline bool rows_fit(int64_t n) { return n <= 4096 && (int64_t)ROWS * (n + 1) * 4 <= SMEM_ROWS_MAX; }
 
@@ -303,6 +368,23 @@ __global__ void __launch_bounds__(256) k_bmm(const float *a, const float *b, flo
 }
 
 // quantize (tensor.py:140-151): clamp(rint(f64 x / f64 scale) + zp, lo, hi)
+__device__ __forceinline__ uint32_t quant1(float x, double scale, int32_t zp, int32_t lo, int32_t hi)
+{
+    double q = rint(__ddiv_rn((double)x, scale)) + (double)zp;
+    q = fmin(fmax(q, (double)lo), (double)hi);
+    return (uint32_t)(uint8_t)(int32_t)q;   // the s8 / u8 byte
+}
+// four elements per thread: 16-byte loads, one 4-byte store
+__global__ void k_quantize4(const float4 *x, int64_t n4, double scale, int32_t zp, int32_t lo, int32_t hi,
+                            uint32_t *out)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 v = __ldg(x + i);
+        out[i] = quant1(v.x, scale, zp, lo, hi) | quant1(v.y, scale, zp, lo, hi) << 8 |
+                 quant1(v.z, scale, zp, lo, hi) << 16 | quant1(v.w, scale, zp, lo, hi) << 24;
+    }
+}
+
 __global__ void k_quantize(const float *x, int64_t n, double scale, int32_t zp, int32_t lo, int32_t hi, void *out,
                            int out_s8)
 {
@@ -346,7 +428,15 @@ extern "C" int32_t si_layer_norm_f32(const float *x, const float *gamma, const f
         return SI_EINVAL;
     }
     if (rows == 0) return SI_OK;
-    if (rows_fit(n)) {
+    const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out) |
+                           reinterpret_cast<uintptr_t>(gamma) | reinterpret_cast<uintptr_t>(beta)) & 15) == 0;
+    if (n % 4 == 0 && aligned && (int64_t)ROWS * (n + 4) * 4 <= SMEM_ROWS_MAX) {   // 84 -> 46 us on config 4
+        const int smem = ROWS * (int)(n + 4) * 4;
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(k_layer_norm_rows_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        k_layer_norm_rows_bulk<<<(unsigned)((rows + ROWS - 1) / ROWS), 32, smem, (cudaStream_t)stream>>>(
+            x, gamma, beta, eps, out, rows, (int)n);
+    } else if (rows_fit(n)) {
         const int smem = ROWS * (int)(n + 1) * 4;
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(k_layer_norm_rows_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -388,7 +478,15 @@ extern "C" int32_t si_quantize_f32(const float *x, int64_t n, float scale, int32
     if (n == 0) return SI_OK;
     const int threads = 256;
     const int64_t blocks = imin64((n + threads - 1) / threads, 148 * 16);
-    k_quantize<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(x, n, (double)scale, zp, lo, hi, out, lo < 0);
+    if (n % 4 == 0 && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
+        const int64_t b4 = imin64((n / 4 + threads - 1) / threads, 148 * 16);
+        k_quantize4<<<(unsigned)b4, threads, 0, (cudaStream_t)stream>>>(reinterpret_cast<const float4 *>(x), n / 4,
+                                                                       (double)scale, zp, lo, hi,
+                                                                       static_cast<uint32_t *>(out));
+    } else {
+        k_quantize<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(x, n, (double)scale, zp, lo, hi, out,
+                                                                           lo < 0);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { si_set_error(cudaGetErrorString(e)); return SI_ECUDA; }
     return SI_OK;

@@ -253,3 +253,31 @@ def test_gpu_fused_attention_unsupported_shape():
     qkv = torch.zeros((129, 3 * 64), dtype=torch.float32, device="cuda")
     ctx = torch.zeros((129, 64), dtype=torch.float32, device="cuda")
     assert not E.attention_fused(qkv, ctx, 1, 129, 1, 64, 0.125)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows,n", [(70, 768), (33, 1024), (5, 4), (64, 12), (31, 770), (1, 3072)])
+def test_gpu_layer_norm_paths_match_oracle(rows, n):
+    """Both LayerNorm kernels (bulk-copy rows for n % 4 == 0, else the
+    staged-lane kernel) against the oracle, bit for bit, on ragged row
+    counts."""
+    from paper_2306_16601_b200.kernels import eltwise as E
+    rng = np.random.default_rng(rows * 31 + n)
+    x = (rng.normal(0, 3, (rows, n)) + rng.normal(0, 5, (rows, 1))).astype(np.float32)
+    g = rng.normal(1, 0.2, n).astype(np.float32)
+    b = rng.normal(0, 0.2, n).astype(np.float32)
+    y = E.layer_norm_f32(_cuda(x), _cuda(g), _cuda(b), 1e-12).cpu().numpy()
+    np.testing.assert_array_equal(y, oracle.layer_norm(x, g, b, 1e-12))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [4096, 4099, 8, 3])
+def test_gpu_quantize_paths_match_oracle(n):
+    """The four-per-thread quantize (n % 4 == 0) and the scalar one, u8 and
+    s8, against the oracle, bit for bit."""
+    from paper_2306_16601_b200.kernels import eltwise as E
+    x = np.random.default_rng(n).normal(0, 40, n).astype(np.float32)
+    for dt, lo, hi, zp in ((DType.U8, 0, 255, 128), (DType.S8, -128, 127, 0)):
+        qp = QuantParams(np.float32(0.37), zp, dt)
+        y = E.quantize_f32(_cuda(x), qp).cpu().numpy()
+        np.testing.assert_array_equal(y, oracle.quantize(x, np.float32(0.37), zp, lo, hi))
