@@ -138,7 +138,7 @@ int32_t si_spmm(const void *host_image, const void *dev_image, const void *x, in
  * spmm.py:283-333): x_host [K, ldx] (SI_ACT_KN) or [N, ldx] (SI_ACT_NK) and
  * out_host [N, ldo] in host memory (pinned for full overlap).  Token chunks
  * of chunk_n are pipelined: H2D of chunk i+1 and D2H of chunk i-1 overlap the
- * kernel on chunk i (launched on `stream`), double-buffered in `workspace`
+ * kernel on chunk i (launched on `stream`), in a 4-deep buffer ring in `workspace`
  * (device, si_spmm_host_workspace_size bytes).  Returns when out_host is
  * complete.  Programs with side inputs: SI_EUNSUPPORTED (use si_spmm). */
 int32_t si_spmm_host_workspace_size(const void *host_image, int64_t chunk_n, int32_t x_layout, int32_t kernel,

@@ -113,7 +113,7 @@ extern "C" int32_t si_spmm(const void *host_image, const void *dev_image, const 
 // The reference's spmm_exec takes host arrays; si_spmm_host is that boundary
 // for callers without device buffers.  Token chunks are pipelined: while the
 // kernel runs on chunk i (caller's stream), chunk i+1 is copied in on one
-// internal stream and chunk i-1 copied out on another, with double-buffered
+// internal stream and chunk i-1 copied out on another, with a 4-deep ring of
 // device chunks in the caller's workspace.  si_spmm_host_batch runs several
 // independent SpMMs (e.g. the Q/K/V projections, or config 5's linear set)
 // as one chunk sequence, so the copy directions of consecutive jobs overlap.
@@ -186,7 +186,11 @@ int32_t check_job(const si_host_job &j, const SiImage *&h)
     return SI_OK;
 }
 
-// workspace: [x 0][x 1][out 0][out 1][kernel], each the max over the jobs
+// workspace: [x 0..RING-1][out 0..RING-1][kernel], each the max over the jobs.
+// A ring deeper than two lets the copy-in stream run ahead of a job whose
+// copy-out is the long direction (5b writes 4x what it reads, 5c the reverse).
+constexpr int RING = 4;
+
 struct BatchLayout {
     uint64_t x_bytes = 0, o_bytes = 0, k_bytes = 0, total = 0;
 };
@@ -206,7 +210,7 @@ int32_t batch_layout(const si_host_job *jobs, int32_t count, int64_t chunk_n, Ba
         B.o_bytes = L.o_bytes > B.o_bytes ? L.o_bytes : B.o_bytes;
         B.k_bytes = L.k_bytes > B.k_bytes ? L.k_bytes : B.k_bytes;
     }
-    B.total = 2 * B.x_bytes + 2 * B.o_bytes + B.k_bytes;
+    B.total = RING * B.x_bytes + RING * B.o_bytes + B.k_bytes;
     return SI_OK;
 }
 
@@ -237,18 +241,25 @@ extern "C" int32_t si_spmm_host_batch(const si_host_job *jobs, int32_t count, vo
         return SI_ECUDA;
     }
     uint8_t *ws = (uint8_t *)workspace;
-    uint8_t *xbuf[2] = {ws, ws + B.x_bytes};
-    uint8_t *obuf[2] = {ws + 2 * B.x_bytes, ws + 2 * B.x_bytes + B.o_bytes};
-    void *kws = B.k_bytes ? ws + 2 * B.x_bytes + 2 * B.o_bytes : nullptr;
+    uint8_t *xbuf[RING], *obuf[RING];
+    for (int r = 0; r < RING; ++r) {
+        xbuf[r] = ws + r * B.x_bytes;
+        obuf[r] = ws + RING * B.x_bytes + r * B.o_bytes;
+    }
+    void *kws = B.k_bytes ? ws + RING * B.x_bytes + RING * B.o_bytes : nullptr;
 
-    cudaEvent_t ev_entry, ev_done, in_done[2], cmp_done[2], out_done[2];
-    cudaEvent_t *all[] = {&ev_entry, &ev_done, &in_done[0], &in_done[1], &cmp_done[0], &cmp_done[1],
-                          &out_done[0], &out_done[1]};
-    for (cudaEvent_t *e : all) cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+    cudaEvent_t ev_entry, ev_done, in_done[RING], cmp_done[RING], out_done[RING];
+    cudaEventCreateWithFlags(&ev_entry, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming);
+    for (int r = 0; r < RING; ++r) {
+        cudaEventCreateWithFlags(&in_done[r], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&cmp_done[r], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&out_done[r], cudaEventDisableTiming);
+    }
     // the workspace may still be in use by work queued earlier on the caller's stream
     cudaEventRecord(ev_entry, s_cmp);
     cudaStreamWaitEvent(s_in, ev_entry, 0);
-    int64_t seq = 0;   // chunk sequence number across the batch (buffer = seq & 1)
+    int64_t seq = 0;   // chunk sequence number across the batch (buffer = seq % RING)
     for (int32_t jb = 0; jb < count && rc == SI_OK; ++jb) {
         const si_host_job &J = jobs[jb];
         const SiImage *h = (const SiImage *)J.host_image;
@@ -257,10 +268,10 @@ extern "C" int32_t si_spmm_host_batch(const si_host_job *jobs, int32_t count, vo
         const uint8_t *xh = (const uint8_t *)J.x_host;
         uint8_t *oh = (uint8_t *)J.out_host;
         for (int64_t n0 = 0; n0 < J.n && rc == SI_OK; n0 += L.chunk, ++seq) {
-            const int b = (int)(seq & 1);
+            const int b = (int)(seq % RING);
             const int64_t nc = J.n - n0 < L.chunk ? J.n - n0 : L.chunk;
-            // copy in: buffer b is free once the kernel two chunks back finished
-            if (seq >= 2) cudaStreamWaitEvent(s_in, cmp_done[b], 0);
+            // copy in: buffer b is free once the kernel RING chunks back finished
+            if (seq >= RING) cudaStreamWaitEvent(s_in, cmp_done[b], 0);
             cudaError_t e;
             if (J.x_layout == SI_ACT_KN)
                 e = cudaMemcpy2DAsync(xbuf[b], (size_t)L.ldx_dev, xh + n0, (size_t)J.ldx, (size_t)nc, (size_t)h->K,
@@ -276,7 +287,7 @@ extern "C" int32_t si_spmm_host_batch(const si_host_job *jobs, int32_t count, vo
             cudaEventRecord(in_done[b], s_in);
             // compute: after its input arrived and the output buffer was drained
             cudaStreamWaitEvent(s_cmp, in_done[b], 0);
-            if (seq >= 2) cudaStreamWaitEvent(s_cmp, out_done[b], 0);
+            if (seq >= RING) cudaStreamWaitEvent(s_cmp, out_done[b], 0);
             rc = si_spmm(J.host_image, J.dev_image, xbuf[b], J.x_layout, L.ldx_dev, nc, nullptr, obuf[b], L.ldo_dev,
                          kws, B.k_bytes, kernel, s_cmp);
             if (rc != SI_OK) break;
@@ -302,7 +313,13 @@ extern "C" int32_t si_spmm_host_batch(const si_host_job *jobs, int32_t count, vo
         rc = SI_ECUDA;
         si_set_error(std::string("host pipeline: ") + cudaGetErrorString(e));
     }
-    for (cudaEvent_t *ev : all) cudaEventDestroy(*ev);
+    cudaEventDestroy(ev_entry);
+    cudaEventDestroy(ev_done);
+    for (int r = 0; r < RING; ++r) {
+        cudaEventDestroy(in_done[r]);
+        cudaEventDestroy(cmp_done[r]);
+        cudaEventDestroy(out_done[r]);
+    }
     return rc;
 }
 
