@@ -9,6 +9,10 @@ tokens, no collective; "scaling": "weak").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
+--gpus N > 1 without a torchrun environment re-launches this script under
+torch.distributed.run with N local ranks (127.0.0.1), so the documented
+command produces the multi-GPU line itself.
+
 Prints ONE JSON line on rank 0.  value = sum(2*nnz*N) over all ranks / the
 max-over-ranks device time of the K timed steps.  Inputs stay in HBM during
 the timed region; every step touches ~768 MB (X and outputs of the three
@@ -39,6 +43,30 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def relaunch_distributed(argv, n: int) -> int:
+    """--gpus N with no WORLD_SIZE in the environment: run N ranks of this
+    script under torch.distributed.run (one process per GPU, NCCL), forward
+    rank 0's JSON line, return the launcher's exit code."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + argv
+    return subprocess.call(cmd)
 
 
 def measured_peaks():
@@ -127,33 +155,65 @@ def cpu_baseline(cells, budget_s: float = 12.0, threads: int | None = None, toke
         if el >= budget_s or reps >= 50:
             break
     return {"value": ops / el / 1e12, "unit": UNIT, "cores": threads, "kind": "port",
+            "cpu_model": cpu_model(),
             "sample": f"config-5 linears on {tokens} tokens x {reps} reps ({el:.1f} s), oracle/si_oracle.c "
                       f"orc_spmm_exec (tiled reference path, bn=64, OpenMP {threads} threads)"}
 
 
 def run_reference(args):
+    """The reference arm: the reference's CPU algorithm for this path
+    (spmm_exec's tiled kernels, spmm.py:192-333, restated in C in oracle/;
+    the reference itself is Python + numba and does not travel to the GPU
+    box) on the SAME workload as our arm -- all three config-5 linears at the
+    full N = 65536 tokens per step -- with every host thread, plus a
+    single-thread sample for the per-core figure."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
+    from oracle import oracle
+    from paper_2306_16601_b200 import encode_sparse, workloads
     cells = make_cells()
+    n = cells[0].n
     threads = len(os.sched_getaffinity(0))
+    prepared = []
+    for c in cells:
+        w, x, bias, scales = workloads.baseline_inputs(c.m, c.k, n, c.ratio, c.seed)
+        sw = encode_sparse(w, scales)
+        prepared.append((c, sw, x, bias, workloads.program(c.program, scales)))
+
+    def step(nthreads, tokens=None):
+        for c, sw, x, bias, prog in prepared:
+            xs = x if tokens is None else np.ascontiguousarray(x[:, :tokens])
+            oracle.spmm_exec(sw, xs, prog, bias, threads=nthreads)
+
     for _ in range(args.warmup):
-        cpu_baseline(cells, budget_s=0.5, threads=threads, tokens=1024)
+        step(threads, tokens=2048)
     t_steps = []
-    ops = 0.0
     for _ in range(args.steps):
-        r = cpu_baseline(cells, budget_s=2.0, threads=threads, tokens=4096)
-        t_steps.append(r)
-    vals = [r["value"] for r in t_steps]
-    value = float(np.mean(vals))
+        t0 = time.perf_counter()
+        step(threads)
+        t_steps.append(time.perf_counter() - t0)
+    ops_step = sum(c.ops(n) for c in cells)
+    sec = float(np.mean(t_steps))
+    value = ops_step / sec / 1e12
+    # one core: a 2048-token slice of the same step
+    t1_tok = 2048
+    t0 = time.perf_counter()
+    step(1, tokens=t1_tok)
+    t1 = time.perf_counter() - t0
+    value_t1 = sum(c.ops(t1_tok) for c in cells) / t1 / 1e12
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8xs8->s32", "data": "synthetic",
-            "config": {"workload": "config5_bert_large_spmm_set", "tokens_sample": 4096,
-                       "linears": [c.name for c in cells], "sparsity": 0.9},
+            "config": {"workload": "config5_bert_large_spmm_set", "tokens_per_rank": n, "global_tokens": n,
+                       "linears": [c.name for c in cells], "sparsity": 0.9,
+                       "epilogue": "bias+requant u8 (scale 2.0, zp 128)"},
             "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": t_steps[-1]["sample"]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "cpu_model": cpu_model(),
+                             "sample": f"the full step (3 linears x {n} tokens) per timed step, oracle/si_oracle.c "
+                                       f"orc_spmm_exec (spmm_exec's tiled path, bn=64), OpenMP {threads} threads",
+                             "single_thread": {"value": value_t1, "unit": UNIT, "cores": 1,
+                                               "sample": f"3 linears x {t1_tok} tokens ({t1:.1f} s)"}},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -165,7 +225,10 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--kernel", default="auto", choices=["auto", "gather", "tc"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "gather", "tc", "sp"])
+    ap.add_argument("--layout", default="nk", choices=["nk", "kn"],
+                    help="activation orientation: nk = token-major [N, K] (relayout_tokens, spmm.py:96; the "
+                         "encoder's layout), kn = [K, N] (relayout_activation, spmm.py:82)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-graphs", action="store_true", help="launch eagerly instead of replaying CUDA graphs")
     ap.add_argument("--e2e-chunk", type=int, default=32768, help="token chunk of the host pipeline")
@@ -176,6 +239,8 @@ def main():
                          "rows of every linear split over the ranks, one NCCL all-gather of the u8 outputs per "
                          "linear (strong scaling, SURVEY 8(e))")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_distributed(sys.argv[1:], args.gpus)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -204,7 +269,11 @@ def main():
         sw = P.encode_sparse(w, scales)
         prog = workloads.program(c.program, scales)
         plan = K.plan_spmm(sw, n, program=prog, bias=bias, device=dev)
-        act = K.relayout_activation(torch.from_numpy(x).pin_memory(), device=dev)
+        if args.layout == "nk":
+            x = np.ascontiguousarray(x.T)   # token-major [N, K]: same values, the transformer layout
+            act = K.relayout_tokens(torch.from_numpy(x).pin_memory(), device=dev)
+        else:
+            act = K.relayout_activation(torch.from_numpy(x).pin_memory(), device=dev)
         out = torch.empty((n, c.m), dtype=torch.uint8, device=dev)
         rs = None
         if rows_mode:
@@ -215,7 +284,8 @@ def main():
         del x
     stream = torch.cuda.current_stream(dev)
     launches_per_step = sum(
-        _lib.lib().si_spmm_launch_count(_lib.ptr(L["plan"].image), n, 0, _lib.KERNELS[args.kernel])
+        _lib.lib().si_spmm_launch_count(_lib.ptr(L["plan"].image), n, _lib.LAYOUTS[args.layout],
+                                        _lib.KERNELS[args.kernel])
         for L in layers)
 
     graphs = []
@@ -306,7 +376,7 @@ def main():
         # host buffers through the C ABI's host entry point (si_spmm_host_batch):
         # the library pipelines copy-in / kernel / copy-out over token chunks
         # of the three independent linears
-        K.spmm_exec_host_batch([(L["plan"], L["x_host"], "kn", outs_host[i]) for i, L in enumerate(layers)],
+        K.spmm_exec_host_batch([(L["plan"], L["x_host"], args.layout, outs_host[i]) for i, L in enumerate(layers)],
                                chunk=args.e2e_chunk)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -331,6 +401,8 @@ def main():
             "config": {"workload": "config5_bert_large_spmm_set", "tokens_per_rank": n,
                        "global_tokens": n if rows_mode else n * world, "linears": [c.name for c in cells], "sparsity": 0.9,
                        "epilogue": "bias+requant u8 (scale 2.0, zp 128)", "kernel": args.kernel,
+                       "activation_layout": ("token-major [N, K] (relayout_tokens)" if args.layout == "nk"
+                                             else "[K, N] (relayout_activation)"),
                        "l2": "no flush: each step touches ~768 MB >> 126 MB L2",
                        "parallelism": (f"row-shard x{world} + NCCL all-gather of the u8 outputs" if rows_mode
                                        else f"token-shard x{world} (no collective)"),

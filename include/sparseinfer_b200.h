@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define SI_ABI_VERSION 1
+#define SI_ABI_VERSION 2  /* 2: side inputs on the host-buffer entry points */
 
 typedef enum {
     SI_OK = 0,
@@ -56,8 +56,9 @@ typedef enum { SI_ACT_KN = 0, SI_ACT_NK = 1 } si_act_layout;
 typedef enum {
     SI_KERNEL_AUTO = 0,
     SI_KERNEL_GATHER = 1,  /* K1: CUDA-core dp4a gather over 4x1 micro-tiles */
-    SI_KERNEL_TC = 2,      /* K2: tcgen05 kind::i8 tensor-core tiles */
-    SI_KERNEL_REF = 3      /* naive per-element kernel (spmm_ref, spmm.py:401) */
+    SI_KERNEL_TC = 2,      /* K2: tcgen05 kind::i8 tensor-core tiles, dense-expanded W */
+    SI_KERNEL_REF = 3,     /* naive per-element kernel (spmm_ref, spmm.py:401) */
+    SI_KERNEL_SP = 4       /* K3: tcgen05.mma.sp 2:4 W images, X-stationary (token-major X, K <= 1024) */
 } si_kernel;
 
 /* Host view of a Sparse4x1Weight (sparse.py:23-41). */
@@ -117,7 +118,9 @@ typedef struct {
 } si_plan_info;
 int32_t si_plan_info_get(const void *host_image, si_plan_info *info);
 
-/* Device workspace the run needs (0 when none). */
+/* Device workspace the run needs (0 when none).  For SI_KERNEL_AUTO this is
+ * enough for either kernel AUTO may pick (the pick also depends on the
+ * alignment of x and ldx, which this query does not see). */
 int32_t si_spmm_workspace_size(const void *host_image, int64_t n, int32_t x_layout,
                                int32_t kernel, uint64_t *bytes);
 
@@ -135,16 +138,21 @@ int32_t si_spmm(const void *host_image, const void *dev_image, const void *x, in
                 void *workspace, uint64_t workspace_bytes, int32_t kernel, void *stream);
 
 /* Host-buffer run (the reference's spmm_exec takes host arrays,
- * spmm.py:283-333): x_host [K, ldx] (SI_ACT_KN) or [N, ldx] (SI_ACT_NK) and
- * out_host [N, ldo] in host memory (pinned for full overlap).  Token chunks
- * of chunk_n are pipelined: H2D of chunk i+1 and D2H of chunk i-1 overlap the
- * kernel on chunk i (launched on `stream`), in a 4-deep buffer ring in `workspace`
- * (device, si_spmm_host_workspace_size bytes).  Returns when out_host is
- * complete.  Programs with side inputs: SI_EUNSUPPORTED (use si_spmm). */
+ * spmm.py:283-333): x_host [K, ldx] (SI_ACT_KN) or [N, ldx] (SI_ACT_NK),
+ * sides_host f32 [n_sides, N, M] (the pack_sides form, epilogue.py:256-263;
+ * NULL when the program has none) and out_host [N, ldo], all in host memory
+ * (pinned for full overlap).  Token chunks of chunk_n are pipelined: H2D of
+ * chunk i+1 and D2H of chunk i-1 overlap the kernel on chunk i (launched on
+ * `stream`), in a 4-deep device buffer ring inside `workspace` (device,
+ * si_spmm_host_workspace_size bytes).  Each call takes its own pair of copy
+ * streams, so concurrent calls with separate workspaces are independent.
+ * Returns when out_host is complete (on error paths too, every copy the call
+ * queued has finished).
+ * replaces spmm_exec, spmm.py:283-333, for callers holding host arrays. */
 int32_t si_spmm_host_workspace_size(const void *host_image, int64_t chunk_n, int32_t x_layout, int32_t kernel,
                                     uint64_t *bytes);
 int32_t si_spmm_host(const void *host_image, const void *dev_image, const void *x_host, int32_t x_layout,
-                     int64_t ldx, int64_t n, void *out_host, int64_t ldo, void *workspace,
+                     int64_t ldx, int64_t n, const float *sides_host, void *out_host, int64_t ldo, void *workspace,
                      uint64_t workspace_bytes, int64_t chunk_n, int32_t kernel, void *stream);
 
 /* Several independent host-buffer SpMMs (e.g. Q/K/V projections) as one
@@ -157,6 +165,7 @@ typedef struct {
     int64_t ldx, n;
     void *out_host;
     int64_t ldo;
+    const float *sides_host;  /* f32 [n_sides, n, M] or NULL (ABI 2) */
 } si_host_job;
 int32_t si_spmm_host_batch_workspace_size(const si_host_job *jobs, int32_t count, int64_t chunk_n,
                                           uint64_t *bytes);

@@ -14,7 +14,7 @@ import numpy as np
 from . import _build
 
 SI_OK, SI_EINVAL, SI_EFORMAT, SI_ECUDA, SI_EUNSUPPORTED, SI_ENOSPACE = range(6)
-KERNELS = {"auto": 0, "gather": 1, "tc": 2, "ref": 3}
+KERNELS = {"auto": 0, "gather": 1, "tc": 2, "ref": 3, "sp": 4}
 LAYOUTS = {"kn": 0, "nk": 1}
 
 _vp, _i32, _i64, _u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
@@ -37,9 +37,12 @@ class SiPlanInfo(ctypes.Structure):
                 ("image_bytes", _u64)]
 
 
+ABI_VERSION = 2   # include/sparseinfer_b200.h SI_ABI_VERSION
+
+
 class SiHostJob(ctypes.Structure):
     _fields_ = [("host_image", _vp), ("dev_image", _vp), ("x_host", _vp), ("x_layout", _i32), ("ldx", _i64),
-                ("n", _i64), ("out_host", _vp), ("ldo", _i64)]
+                ("n", _i64), ("out_host", _vp), ("ldo", _i64), ("sides_host", _vp)]
 
 
 _lib = None
@@ -67,7 +70,7 @@ def lib():
     L.si_spmm_launch_count.argtypes = [_vp, _i64, _i32, _i32]
     L.si_spmm.argtypes = [_vp, _vp, _vp, _i32, _i64, _i64, _vp, _vp, _i64, _vp, _u64, _i32, _vp]
     L.si_spmm_host_workspace_size.argtypes = [_vp, _i64, _i32, _i32, ctypes.POINTER(_u64)]
-    L.si_spmm_host.argtypes = [_vp, _vp, _vp, _i32, _i64, _i64, _vp, _i64, _vp, _u64, _i64, _i32, _vp]
+    L.si_spmm_host.argtypes = [_vp, _vp, _vp, _i32, _i64, _i64, _vp, _vp, _i64, _vp, _u64, _i64, _i32, _vp]
     L.si_spmm_host_batch_workspace_size.argtypes = [ctypes.POINTER(SiHostJob), _i32, _i64, ctypes.POINTER(_u64)]
     L.si_spmm_host_batch.argtypes = [ctypes.POINTER(SiHostJob), _i32, _vp, _u64, _i64, _i32, _vp]
     L.si_softmax_rows_f32.argtypes = [_vp, _vp, _i64, _i64, _vp]
@@ -81,7 +84,7 @@ def lib():
               "si_spmm_host_batch_workspace_size", "si_spmm_host_batch",
               "si_softmax_rows_f32", "si_layer_norm_f32", "si_bmm_f32", "si_quantize_f32", "si_attention_f32"):
         getattr(L, f).restype = _i32
-    if L.si_abi_version() != 1:
+    if L.si_abi_version() != ABI_VERSION:
         raise RuntimeError("libsparseinfer_b200 ABI version mismatch")
     _lib = L
     return L

@@ -3,11 +3,13 @@
 // Replaces spmm_exec (spmm.py:283-333): the reference validates the plan
 // against the activation and picks a task kernel by the program's output
 // dtype, then fans tasks out on its thread pool; here the plan image picks
-// the epilogue form and the shape picks K1 (gather, CUDA cores) or K2
-// (tcgen05 tensor-core tiles).  All launches are on the caller's stream.
+// the epilogue form and the shape picks K1 (gather, CUDA cores), K3 (2:4
+// sparse tensor cores, X-stationary) or K2 (dense-expanded tensor-core
+// tiles).  All launches are on the caller's stream.
 #include <cuda_runtime.h>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/sparseinfer_b200.h"
 #include "si_internal.h"
@@ -29,12 +31,18 @@ int32_t pick_kernel(const SiImage *h, int64_t n, int32_t layout, int32_t kernel,
 {
     if (kernel != SI_KERNEL_AUTO) return kernel;
     // tensor cores whenever TMA-legal, except tiny weights at small N where
-    // the gather kernel's single wave is shorter; measured over all 140
-    // config-2 cells with CUDA-graph replay (profiles/r01b_config2_*.md,
-    // DESIGN.md "Kernel selection")
-    if ((n >= 1024 || (int64_t)h->M * h->K >= (1 << 18)) && k2_supported(h, n, layout, x, ldx, ldo))
-        return SI_KERNEL_TC;
+    // the gather kernel's single wave is shorter (all 140 config-2 cells,
+    // CUDA-graph replay: profiles/r01b_config2_*.md, DESIGN.md "Kernel
+    // selection")
+    if (n >= 1024 || (int64_t)h->M * h->K >= (1 << 18)) {
+        if (k2_supported(h, n, layout, x, ldx, ldo)) return SI_KERNEL_TC;
+    }
     return SI_KERNEL_GATHER;
+}
+
+uint64_t kernel_workspace(const SiImage *h, int64_t n, int32_t layout, int32_t k)
+{
+    return k == SI_KERNEL_GATHER ? k1_workspace(h, n, layout) : k == SI_KERNEL_TC ? k2_workspace(h, n, layout) : 0;
 }
 
 }  // namespace
@@ -44,10 +52,19 @@ extern "C" int32_t si_spmm_workspace_size(const void *host_image, int64_t n, int
 {
     const SiImage *h = check_image(host_image);
     if (!h) return SI_EINVAL;
-    int32_t k = pick_kernel(h, n, x_layout, kernel, nullptr, x_layout == SI_ACT_KN ? n : h->K, h->M);
-    *bytes = k == SI_KERNEL_GATHER ? k1_workspace(h, n, x_layout)
-           : k == SI_KERNEL_TC     ? k2_workspace(h, n, x_layout)
-                                   : 0;
+    if (!bytes) {
+        si_set_error("null output pointer");
+        return SI_EINVAL;
+    }
+    if (kernel == SI_KERNEL_AUTO) {
+        // AUTO falls back to K1 for activations the tensor-core kernels cannot
+        // read (unaligned base or leading dimension), which this query cannot
+        // see: report what either kernel needs
+        const uint64_t k1 = k1_workspace(h, n, x_layout), k2 = k2_workspace(h, n, x_layout);
+        *bytes = k1 > k2 ? k1 : k2;
+        return SI_OK;
+    }
+    *bytes = kernel_workspace(h, n, x_layout, kernel);
     return SI_OK;
 }
 
@@ -56,9 +73,7 @@ extern "C" int32_t si_spmm_launch_count(const void *host_image, int64_t n, int32
     const SiImage *h = check_image(host_image);
     if (!h) return -1;
     int32_t k = pick_kernel(h, n, x_layout, kernel, nullptr, x_layout == SI_ACT_KN ? n : h->K, h->M);
-    return k == SI_KERNEL_GATHER ? k1_launch_count(h, x_layout)
-         : k == SI_KERNEL_TC     ? k2_launch_count(h, x_layout)
-                                 : 1;
+    return k == SI_KERNEL_GATHER ? k1_launch_count(h, x_layout) : k == SI_KERNEL_TC ? k2_launch_count(h, x_layout) : 1;
 }
 
 extern "C" int32_t si_spmm(const void *host_image, const void *dev_image, const void *x, int32_t x_layout,
@@ -87,10 +102,12 @@ extern "C" int32_t si_spmm(const void *host_image, const void *dev_image, const 
         si_set_error("program needs side inputs");
         return SI_EINVAL;
     }
+    if (kernel < SI_KERNEL_AUTO || kernel > SI_KERNEL_SP) {
+        si_set_error("unknown kernel id");
+        return SI_EINVAL;
+    }
     int32_t k = pick_kernel(h, n, x_layout, kernel, x, ldx, ldo);
-    uint64_t need = k == SI_KERNEL_GATHER ? k1_workspace(h, n, x_layout)
-                  : k == SI_KERNEL_TC     ? k2_workspace(h, n, x_layout)
-                                          : 0;
+    uint64_t need = kernel_workspace(h, n, x_layout, k);
     if (workspace_bytes < need || (need && !workspace)) {
         si_set_error("workspace too small: need " + std::to_string(need) + " bytes");
         return SI_ENOSPACE;
@@ -99,9 +116,16 @@ extern "C" int32_t si_spmm(const void *host_image, const void *dev_image, const 
         si_set_error("tensor-core kernel does not support this shape/layout");
         return SI_EUNSUPPORTED;
     }
+    if (k == SI_KERNEL_SP && !k3_supported(h, n, x_layout, x, ldx)) {
+        si_set_error("2:4 kernel needs token-major 16-byte-aligned activations, K <= 1024, >= 2 row tiles");
+        return SI_EUNSUPPORTED;
+    }
     SpmmArgs a{h, dev_image, (const uint8_t *)x, x_layout, ldx, n, sides, out, ldo, workspace, workspace_bytes,
                stream};
-    int err = k == SI_KERNEL_GATHER ? k1_launch(a) : k == SI_KERNEL_TC ? k2_launch(a) : kref_launch(a);
+    int err = k == SI_KERNEL_GATHER ? k1_launch(a)
+            : k == SI_KERNEL_TC     ? k2_launch(a)
+            : k == SI_KERNEL_SP     ? k3_launch(a)
+                                    : kref_launch(a);
     if (err != cudaSuccess) {
         si_set_error(std::string("CUDA launch failed: ") + cudaGetErrorString((cudaError_t)err));
         return SI_ECUDA;
@@ -143,24 +167,42 @@ HostLayout host_layout(const SiImage *h, int64_t chunk_n, int32_t x_layout)
     return L;
 }
 
+// Copy streams for the host pipeline come from a per-device pool: a call
+// takes a private pair for its duration, so concurrent host-buffer calls
+// (each with its own workspace) never share an in-flight copy stream.
+struct CopyStreams {
+    int dev = -1;
+    cudaStream_t in = nullptr, out = nullptr;
+};
 std::mutex g_stream_mu;
-cudaStream_t g_copy_streams[64][2];
-bool g_copy_init[64];
+std::vector<CopyStreams> g_stream_pool;
 
-bool copy_streams(cudaStream_t &in, cudaStream_t &out)
+bool acquire_copy_streams(CopyStreams &cs)
 {
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return false;
-    std::lock_guard<std::mutex> lk(g_stream_mu);
-    if (!g_copy_init[dev]) {
-        if (cudaStreamCreateWithFlags(&g_copy_streams[dev][0], cudaStreamNonBlocking) != cudaSuccess ||
-            cudaStreamCreateWithFlags(&g_copy_streams[dev][1], cudaStreamNonBlocking) != cudaSuccess)
-            return false;
-        g_copy_init[dev] = true;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    {
+        std::lock_guard<std::mutex> lk(g_stream_mu);
+        for (size_t i = 0; i < g_stream_pool.size(); ++i)
+            if (g_stream_pool[i].dev == dev) {
+                cs = g_stream_pool[i];
+                g_stream_pool.erase(g_stream_pool.begin() + (long)i);
+                return true;
+            }
     }
-    in = g_copy_streams[dev][0];
-    out = g_copy_streams[dev][1];
+    cs.dev = dev;
+    if (cudaStreamCreateWithFlags(&cs.in, cudaStreamNonBlocking) != cudaSuccess) return false;
+    if (cudaStreamCreateWithFlags(&cs.out, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaStreamDestroy(cs.in);
+        return false;
+    }
     return true;
+}
+
+void release_copy_streams(const CopyStreams &cs)
+{
+    std::lock_guard<std::mutex> lk(g_stream_mu);
+    g_stream_pool.push_back(cs);
 }
 
 int32_t check_job(const si_host_job &j, const SiImage *&h)
@@ -179,21 +221,39 @@ int32_t check_job(const si_host_job &j, const SiImage *&h)
         si_set_error("leading dimension smaller than the row");
         return SI_EINVAL;
     }
-    if (h->n_sides > 0) {
-        si_set_error("host-buffer entry point does not take side inputs (use si_spmm)");
-        return SI_EUNSUPPORTED;
+    if (h->n_sides > 0 && !j.sides_host) {
+        si_set_error("program needs side inputs");
+        return SI_EINVAL;
     }
     return SI_OK;
 }
 
-// workspace: [x 0..RING-1][out 0..RING-1][kernel], each the max over the jobs.
+// workspace: [x 0..RING-1][out 0..RING-1][sides 0..RING-1][kernel], each the
+// max over the jobs.
 // A ring deeper than two lets the copy-in stream run ahead of a job whose
 // copy-out is the long direction (5b writes 4x what it reads, 5c the reverse).
 constexpr int RING = 4;
 
 struct BatchLayout {
-    uint64_t x_bytes = 0, o_bytes = 0, k_bytes = 0, total = 0;
+    uint64_t x_bytes = 0, o_bytes = 0, s_bytes = 0, k_bytes = 0, total = 0;
 };
+
+// per-chunk side-input buffer: f32 [n_sides][chunk][M]
+uint64_t side_bytes(const SiImage *h, int64_t chunk)
+{
+    return align_up((uint64_t)h->n_sides * (uint64_t)chunk * (uint64_t)h->M * 4, WS_ALIGN);
+}
+
+void add_job_layout(const SiImage *h, int64_t chunk_n, int32_t x_layout, BatchLayout &B)
+{
+    const HostLayout L = host_layout(h, chunk_n, x_layout);
+    const uint64_t sb = side_bytes(h, L.chunk);
+    B.x_bytes = L.x_bytes > B.x_bytes ? L.x_bytes : B.x_bytes;
+    B.o_bytes = L.o_bytes > B.o_bytes ? L.o_bytes : B.o_bytes;
+    B.s_bytes = sb > B.s_bytes ? sb : B.s_bytes;
+    B.k_bytes = L.k_bytes > B.k_bytes ? L.k_bytes : B.k_bytes;
+    B.total = RING * (B.x_bytes + B.o_bytes + B.s_bytes) + B.k_bytes;
+}
 
 int32_t batch_layout(const si_host_job *jobs, int32_t count, int64_t chunk_n, BatchLayout &B)
 {
@@ -205,12 +265,8 @@ int32_t batch_layout(const si_host_job *jobs, int32_t count, int64_t chunk_n, Ba
         const SiImage *h = nullptr;
         int32_t rc = check_job(jobs[i], h);
         if (rc != SI_OK) return rc;
-        const HostLayout L = host_layout(h, chunk_n, jobs[i].x_layout);
-        B.x_bytes = L.x_bytes > B.x_bytes ? L.x_bytes : B.x_bytes;
-        B.o_bytes = L.o_bytes > B.o_bytes ? L.o_bytes : B.o_bytes;
-        B.k_bytes = L.k_bytes > B.k_bytes ? L.k_bytes : B.k_bytes;
+        add_job_layout(h, chunk_n, jobs[i].x_layout, B);
     }
-    B.total = RING * B.x_bytes + RING * B.o_bytes + B.k_bytes;
     return SI_OK;
 }
 
@@ -235,22 +291,27 @@ extern "C" int32_t si_spmm_host_batch(const si_host_job *jobs, int32_t count, vo
         si_set_error("workspace too small: need " + std::to_string(B.total) + " bytes");
         return SI_ENOSPACE;
     }
-    cudaStream_t s_cmp = (cudaStream_t)stream, s_in, s_out;
-    if (!copy_streams(s_in, s_out)) {
+    cudaStream_t s_cmp = (cudaStream_t)stream;
+    CopyStreams cs;
+    if (!acquire_copy_streams(cs)) {
         si_set_error("cannot create copy streams");
         return SI_ECUDA;
     }
+    cudaStream_t s_in = cs.in, s_out = cs.out;
     uint8_t *ws = (uint8_t *)workspace;
     uint8_t *xbuf[RING], *obuf[RING];
+    float *sbuf[RING];
     for (int r = 0; r < RING; ++r) {
         xbuf[r] = ws + r * B.x_bytes;
         obuf[r] = ws + RING * B.x_bytes + r * B.o_bytes;
+        sbuf[r] = (float *)(ws + RING * (B.x_bytes + B.o_bytes) + r * B.s_bytes);
     }
-    void *kws = B.k_bytes ? ws + RING * B.x_bytes + RING * B.o_bytes : nullptr;
+    void *kws = B.k_bytes ? ws + RING * (B.x_bytes + B.o_bytes + B.s_bytes) : nullptr;
 
-    cudaEvent_t ev_entry, ev_done, in_done[RING], cmp_done[RING], out_done[RING];
+    cudaEvent_t ev_entry, ev_in_end, ev_out_end, in_done[RING], cmp_done[RING], out_done[RING];
     cudaEventCreateWithFlags(&ev_entry, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_in_end, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_out_end, cudaEventDisableTiming);
     for (int r = 0; r < RING; ++r) {
         cudaEventCreateWithFlags(&in_done[r], cudaEventDisableTiming);
         cudaEventCreateWithFlags(&cmp_done[r], cudaEventDisableTiming);
@@ -267,6 +328,7 @@ extern "C" int32_t si_spmm_host_batch(const si_host_job *jobs, int32_t count, vo
         const int eb = out_elem_bytes(h);
         const uint8_t *xh = (const uint8_t *)J.x_host;
         uint8_t *oh = (uint8_t *)J.out_host;
+        const int ns = h->n_sides;
         for (int64_t n0 = 0; n0 < J.n && rc == SI_OK; n0 += L.chunk, ++seq) {
             const int b = (int)(seq % RING);
             const int64_t nc = J.n - n0 < L.chunk ? J.n - n0 : L.chunk;
@@ -279,6 +341,11 @@ extern "C" int32_t si_spmm_host_batch(const si_host_job *jobs, int32_t count, vo
             else
                 e = cudaMemcpy2DAsync(xbuf[b], (size_t)L.ldx_dev, xh + n0 * J.ldx, (size_t)J.ldx, (size_t)h->K,
                                       (size_t)nc, cudaMemcpyHostToDevice, s_in);
+            // side inputs: rows n0 .. n0+nc of each [N, M] side, packed [ns][nc][M]
+            for (int sd = 0; sd < ns && e == cudaSuccess; ++sd)
+                e = cudaMemcpyAsync(sbuf[b] + (size_t)sd * nc * h->M,
+                                    J.sides_host + ((size_t)sd * J.n + n0) * h->M, (size_t)nc * h->M * 4,
+                                    cudaMemcpyHostToDevice, s_in);
             if (e != cudaSuccess) {
                 rc = SI_ECUDA;
                 si_set_error(std::string("H2D: ") + cudaGetErrorString(e));
@@ -288,8 +355,8 @@ extern "C" int32_t si_spmm_host_batch(const si_host_job *jobs, int32_t count, vo
             // compute: after its input arrived and the output buffer was drained
             cudaStreamWaitEvent(s_cmp, in_done[b], 0);
             if (seq >= RING) cudaStreamWaitEvent(s_cmp, out_done[b], 0);
-            rc = si_spmm(J.host_image, J.dev_image, xbuf[b], J.x_layout, L.ldx_dev, nc, nullptr, obuf[b], L.ldo_dev,
-                         kws, B.k_bytes, kernel, s_cmp);
+            rc = si_spmm(J.host_image, J.dev_image, xbuf[b], J.x_layout, L.ldx_dev, nc, ns ? sbuf[b] : nullptr,
+                         obuf[b], L.ldo_dev, kws, B.k_bytes, kernel, s_cmp);
             if (rc != SI_OK) break;
             cudaEventRecord(cmp_done[b], s_cmp);
             // copy out
@@ -304,17 +371,23 @@ extern "C" int32_t si_spmm_host_batch(const si_host_job *jobs, int32_t count, vo
             cudaEventRecord(out_done[b], s_out);
         }
     }
-    // host outputs are complete when this returns; later work on the caller's
-    // stream is ordered after the last copy
-    cudaEventRecord(ev_done, s_out);
-    cudaStreamWaitEvent(s_cmp, ev_done, 0);
-    cudaError_t e = cudaStreamSynchronize(s_out);
-    if (rc == SI_OK && e != cudaSuccess) {
+    // join both copy streams -- on the error paths too, so no copy queued by
+    // this call still touches the caller's host buffers or the workspace once
+    // it returns; later work on the caller's stream is ordered after them
+    cudaEventRecord(ev_in_end, s_in);
+    cudaEventRecord(ev_out_end, s_out);
+    cudaStreamWaitEvent(s_cmp, ev_in_end, 0);
+    cudaStreamWaitEvent(s_cmp, ev_out_end, 0);
+    const cudaError_t e_in = cudaStreamSynchronize(s_in);
+    const cudaError_t e_out = cudaStreamSynchronize(s_out);
+    if (rc == SI_OK && (e_in != cudaSuccess || e_out != cudaSuccess)) {
         rc = SI_ECUDA;
-        si_set_error(std::string("host pipeline: ") + cudaGetErrorString(e));
+        si_set_error(std::string("host pipeline: ") + cudaGetErrorString(e_in != cudaSuccess ? e_in : e_out));
     }
+    release_copy_streams(cs);
     cudaEventDestroy(ev_entry);
-    cudaEventDestroy(ev_done);
+    cudaEventDestroy(ev_in_end);
+    cudaEventDestroy(ev_out_end);
     for (int r = 0; r < RING; ++r) {
         cudaEventDestroy(in_done[r]);
         cudaEventDestroy(cmp_done[r]);
@@ -333,15 +406,18 @@ extern "C" int32_t si_spmm_host_workspace_size(const void *host_image, int64_t c
         si_set_error("bad chunk size, layout or output pointer");
         return SI_EINVAL;
     }
-    const HostLayout L = host_layout(h, chunk_n, x_layout);
-    *bytes = 2 * L.x_bytes + 2 * L.o_bytes + L.k_bytes;
+    // the same layout si_spmm_host_batch uses for a one-job batch
+    BatchLayout B;
+    add_job_layout(h, chunk_n, x_layout, B);
+    *bytes = B.total;
     return SI_OK;
 }
 
 extern "C" int32_t si_spmm_host(const void *host_image, const void *dev_image, const void *x_host, int32_t x_layout,
-                                int64_t ldx, int64_t n, void *out_host, int64_t ldo, void *workspace,
-                                uint64_t workspace_bytes, int64_t chunk_n, int32_t kernel, void *stream)
+                                int64_t ldx, int64_t n, const float *sides_host, void *out_host, int64_t ldo,
+                                void *workspace, uint64_t workspace_bytes, int64_t chunk_n, int32_t kernel,
+                                void *stream)
 {
-    const si_host_job j{host_image, dev_image, x_host, x_layout, ldx, n, out_host, ldo};
+    const si_host_job j{host_image, dev_image, x_host, x_layout, ldx, n, out_host, ldo, sides_host};
     return si_spmm_host_batch(&j, 1, workspace, workspace_bytes, chunk_n, kernel, stream);
 }

@@ -685,11 +685,8 @@ extern "C" int32_t si_attention_f32(const float *qkv, float *ctx, int64_t batch,
     }
     if (batch == 0) return SI_OK;
     const int smem = AT_SMEM;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
+    // (cheap; set on every call so every device of the process has it)
+    cudaFuncSetAttribute(k_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k_attention<<<(unsigned)(batch * heads), 256, smem, (cudaStream_t)stream>>>(qkv, ctx, seq, heads, head_dim, ld_qkv,
                                                                                ld_ctx, alpha);
     cudaError_t e = cudaGetLastError();

@@ -1,4 +1,4 @@
-// k2_common.cuh -- shared by the tensor-core kernels (spmm_tc.cu, spmm_tcx.cu):
+// k2_common.cuh -- shared by the tensor-core kernels (spmm_tc.cu, spmm_xs.cu):
 // tile constants, kernel parameters, the compiled epilogue forms of the
 // reference's _run_chain (epilogue.py:207-249) and the host-side launch helpers.
 #pragma once
@@ -9,6 +9,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <set>
+#include <utility>
 #include <string>
 
 #include "epilogue.cuh"
@@ -39,27 +41,19 @@ constexpr int STG_BYTES = EPI_GROUPS * STG_GROUP;
 constexpr int TABLE_BYTES = 16 * 1024;      // breakpoint tables staged in smem (EPI_DEQ_TABLE)
 constexpr int SMEM_MAX = 232448;
 
-enum OutKind { OUT_32 = 0, OUT_U8_TMA = 1, OUT_S8_TMA = 2, OUT_8_DIRECT = 3, OUT_U8_Q = 4, OUT_S8_Q = 5 };
+enum OutKind { OUT_32 = 0, OUT_U8_TMA = 1, OUT_S8_TMA = 2, OUT_8_DIRECT = 3 };
 
 struct K2Params {
     int32_t mtiles;      // weight-row tiles (128 rows single-CTA, 256 rows per pair)
     int32_t ntiles;      // 256-token tiles
-    int32_t kchunks;     // K / 128
+    int32_t kchunks;     // k stages
     int32_t b_mn_major;  // 1: X is [K, N] (MN-major B), 0: [N, K] (K-major B)
-    int32_t mgroups;     // pair X-stationary: m-tiles split into this many work units per token tile
     int64_t N;
     void *out;
     int64_t ldo;
     const float *rqc;    // requant c[m] = f32(scale_in[m] / fp)
     const float *rqg;    // per-row class (image off_rqg): < 0 unsafe, >= 1 proven, else requant guard
     const float *rqp;    // proven rows' requant multiplier (image off_rqp)
-    int32_t rtiles;      // 128-row weight tiles with expansion lists (k2x)
-    const uint8_t *x;    // K2s residual: activations [K][ldx] (KN layout)
-    int64_t ldx;
-    const int32_t *sp_rptr;  // K2s residual entry offsets per padded row
-    const int32_t *sp_res;   // K2s residual entries (k << 8) | (uint8)w
-    int32_t debug;       // experiment switches (SI_K2_DEBUG): 1 skip epilogue, 2 W tile 0 only,
-                         // 4 X tile 0 only, 8 no TMA, 16 no MMA
 };
 
 constexpr float MAGIC_F = 12582912.0f;     // 1.5 * 2^23
@@ -106,51 +100,19 @@ struct NoOp {
     __device__ __forceinline__ void operator()() const {}
 };
 
-// on_loaded() runs once the chunk's accumulators are in registers (K2a
-// releases the TMEM accumulator there, before the math and the stores).
-template <int MODE, int OUTK, bool RES = false, typename OnLoaded = NoOp>
+// on_loaded() runs once the chunk's accumulators are in registers (the
+// accumulator can be released there, before the math and the stores).
+template <int MODE, int OUTK, typename OnLoaded = NoOp>
 __device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, int32_t adj, float s_in, float cq,
                                           float gm, bool fast, int64_t n0, int c, const K2Params &P,
-                                          const EpiParams &E, const EpiWarp &W, int32_t rp0 = 0, int32_t rp1 = 0,
-                                          OnLoaded on_loaded = OnLoaded())
+                                          const EpiParams &E, const EpiWarp &W, OnLoaded on_loaded = OnLoaded())
 {
     uint32_t r[32];
     tc::tmem_ld_32x32b_x32(taddr, r);
     tc::tmem_ld_wait();
     on_loaded();
-    if constexpr (RES) {
-        // K2s: block columns that did not fit the 2:4 operand (windows with
-        // more than two nonzero columns), w * X[k][n0 .. n0+31] per entry
-#pragma unroll 1
-        for (int32_t e = rp0; e < ((P.debug & 512) ? rp0 : rp1); ++e) {
-            const int32_t ent = __ldg(P.sp_res + e);
-            const uint32_t w = (uint32_t)(int32_t)(int8_t)(ent & 0xFF);
-            const uint8_t *xp = P.x + (int64_t)(ent >> 8) * P.ldx + n0;
-            uint32_t xw[8];
-            if (n0 + 32 <= P.N) {
-                const uint4 a0 = __ldg(reinterpret_cast<const uint4 *>(xp));
-                const uint4 a1 = __ldg(reinterpret_cast<const uint4 *>(xp) + 1);
-                xw[0] = a0.x; xw[1] = a0.y; xw[2] = a0.z; xw[3] = a0.w;
-                xw[4] = a1.x; xw[5] = a1.y; xw[6] = a1.z; xw[7] = a1.w;
-            } else {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    xw[i] = 0;
-#pragma unroll
-                    for (int b = 0; b < 4; ++b)
-                        if (n0 + 4 * i + b < P.N) xw[i] |= (uint32_t)xp[4 * i + b] << (8 * b);
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < 32; ++j) r[j] += w * ((xw[j >> 2] >> (8 * (j & 3))) & 0xFFu);
-        }
-    }
     int32_t v[32];
-    if (P.debug & 32768) {
-        // experiment: trivial math, same packing / staging / stores
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = (int32_t)(r[j] + (uint32_t)adj);
-    } else if constexpr (MODE == EPI_REQUANT) {
+    if constexpr (MODE == EPI_REQUANT) {
         const int32_t adjM = (int32_t)((uint32_t)adj + (uint32_t)MAGIC_I);
         const int32_t qoff = MAGIC_I - E.q_zp;
         float emax = 0.0f;
@@ -318,32 +280,6 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, i
             for (int j = 0; j < 32; ++j)
                 if (n0 + j < P.N) reinterpret_cast<uint8_t *>(P.out)[(n0 + j) * P.ldo + m] = (uint8_t)(v[j] & 0xFF);
         }
-    } else if constexpr (OUTK == OUT_U8_Q || OUTK == OUT_S8_Q) {
-        // saturating pack of 4 consecutive tokens, quad transpose to 4
-        // consecutive m, one 32-bit store per 4 outputs: each warp store
-        // covers 4 token rows x 32 contiguous bytes (full sectors)
-        const int32_t mq = m - W.lane + 4 * W.i4;
-        uint8_t *o8 = reinterpret_cast<uint8_t *>(P.out);
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-            uint32_t word;
-            if (OUTK == OUT_U8_Q)
-                word = tc::pack_sat_u8(v[4 * w + 1], v[4 * w], tc::pack_sat_u8(v[4 * w + 3], v[4 * w + 2], 0));
-            else
-                word = tc::pack_sat_s8(v[4 * w + 1], v[4 * w], tc::pack_sat_s8(v[4 * w + 3], v[4 * w + 2], 0));
-            word = quad_transpose(word, W.selA, W.selB);
-            const int64_t n = n0 + 4 * w + W.u;
-            if (n < P.N) {
-                uint8_t *dst = o8 + n * P.ldo + mq;
-                if (mq + 3 < E.M) {
-                    *reinterpret_cast<uint32_t *>(dst) = word;
-                } else {
-#pragma unroll
-                    for (int b = 0; b < 4; ++b)
-                        if (mq + b < E.M) dst[b] = (uint8_t)(word >> (8 * b));
-                }
-            }
-        }
     } else {
         // saturating pack of 4 consecutive tokens, quad transpose to 4
         // consecutive m, swizzled STS into the [token][128 m] staging tile
@@ -367,7 +303,7 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, i
 // followed by the release of the accumulator and (8-bit) the TMA store of
 // the group's staging tile.  row0 = first weight row of this CTA's 128-row
 // half, tmem_col = accumulator column base.  release(): arrive on tempty.
-template <int MODE, int OUTK, bool RES = false, typename Wait, typename Release>
+template <int MODE, int OUTK, typename Wait, typename Release>
 __device__ __forceinline__ void epi_tile(uint32_t tmem_base, uint32_t tmem_col, int32_t row0, int64_t tok0,
                                          const CUtensorMap *tmap_o, const K2Params &P, const EpiParams &E,
                                          const EpiWarp &W, Wait wait_full, Release release)
@@ -387,15 +323,11 @@ __device__ __forceinline__ void epi_tile(uint32_t tmem_base, uint32_t tmem_col, 
     // gm: 1 (2: I2F conversion) when every row of the warp is proven exact
     // (no certificate), else this row's certificate guard (proven rows: 0);
     // fast: every row stays inside the magic-number range
-    const bool proven = !(P.debug & 256) && __all_sync(0xffffffffu, gr >= 1.0f);
+    const bool proven = __all_sync(0xffffffffu, gr >= 1.0f);
     const bool wide = __any_sync(0xffffffffu, gr >= 2.0f);
-    const bool fast = !(P.debug & 256) && !wide && __all_sync(0xffffffffu, gr >= 0.0f);
+    const bool fast = !wide && __all_sync(0xffffffffu, gr >= 0.0f);
     const float gm = proven ? (wide ? 2.0f : 1.0f) : (gr >= 1.0f ? 0.0f : fmaxf(gr, 0.0f));
     if (proven) cq = cp;
-    int32_t rp0 = 0, rp1 = 0;
-    if constexpr (RES) {
-        if (mok) { rp0 = __ldg(P.sp_rptr + m); rp1 = __ldg(P.sp_rptr + m + 1); }
-    }
     wait_full();
     tc::tc_fence_after();
     if constexpr (STAGED) {
@@ -403,47 +335,27 @@ __device__ __forceinline__ void epi_tile(uint32_t tmem_base, uint32_t tmem_col, 
         if (W.q == 2 && W.lane == 0) tc::tma_store_wait_read0();
         tc::named_bar_sync(1 + W.g, 128);
     }
-    if (P.debug & 16384) {
-        // experiment: TMEM loads only (no math, no stores)
-        uint32_t acc = 0;
-#pragma unroll 1
-        for (int c = 0; c < COLS / 32; ++c) {
-            uint32_t r[32];
-            tc::tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(W.q * 32) << 16) + tmem_col + W.g * COLS + c * 32, r);
-            tc::tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 32; ++j) acc ^= r[j];
-        }
-        if (acc == 0x12345678u && m == -1) reinterpret_cast<uint32_t *>(P.out)[0] = acc;
-    } else if (!(P.debug & 1)) {
-        // the accumulator is released as soon as the last chunk is in
-        // registers (before its math and staging), so the MMAs of the tile
-        // after next can start that much earlier
-        auto rel = [&]() {
-            tc::tc_fence_before();
-            __syncwarp();
-            if (W.lane == 0) release();
-        };
-#pragma unroll 1
-        for (int c = 0; c < COLS / 32; ++c) {
-            const int col = W.g * COLS + c * 32;
-            const uint32_t ta = tmem_base + ((uint32_t)(W.q * 32) << 16) + tmem_col + col;
-            if (c == COLS / 32 - 1)
-                epi_chunk<MODE, OUTK, RES>(ta, m, mok, adj, s_in, cq, gm, fast, tok0 + col, c, P, E, W, rp0, rp1, rel);
-            else
-                epi_chunk<MODE, OUTK, RES>(ta, m, mok, adj, s_in, cq, gm, fast, tok0 + col, c, P, E, W, rp0, rp1);
-        }
-    }
-    if (P.debug & (1 | 16384)) {
-        // (experiments) this warp's TMEM reads are complete: release the accumulator
+    // the accumulator is released as soon as the last chunk is in registers
+    // (before its math and staging), so the MMAs of the tile after next can
+    // start that much earlier
+    auto rel = [&]() {
         tc::tc_fence_before();
         __syncwarp();
         if (W.lane == 0) release();
+    };
+#pragma unroll 1
+    for (int c = 0; c < COLS / 32; ++c) {
+        const int col = W.g * COLS + c * 32;
+        const uint32_t ta = tmem_base + ((uint32_t)(W.q * 32) << 16) + tmem_col + col;
+        if (c == COLS / 32 - 1)
+            epi_chunk<MODE, OUTK>(ta, m, mok, adj, s_in, cq, gm, fast, tok0 + col, c, P, E, W, rel);
+        else
+            epi_chunk<MODE, OUTK>(ta, m, mok, adj, s_in, cq, gm, fast, tok0 + col, c, P, E, W);
     }
     if constexpr (STAGED) {
         tc::fence_proxy_async_smem();
         tc::named_bar_sync(1 + W.g, 128);
-        if (W.q == 2 && W.lane == 0 && !(P.debug & 8192)) {   // 8192: experiment, no output store
+        if (W.q == 2 && W.lane == 0) {
             tc::tma_store_2d(tmap_o, W.stg, row0, (int32_t)(tok0 + W.g * COLS));
             tc::tma_store_commit();
         }
@@ -552,36 +464,19 @@ bool encode_3d_kblocks(CUtensorMap *m, const void *ptr, uint64_t n, uint64_t k, 
     return r == CUDA_SUCCESS;
 }
 
-int env_int(const char *name, int dflt)
+// the dynamic shared-memory limit is a property of (function, device): set
+// once per (kernel, device), under a lock (every instantiation of a kernel
+// template has the same pointer type, so the key is the pointer value)
+template <typename Kern>
+void set_smem_attr(Kern kern, int smem)
 {
-    const char *e = getenv(name);
-    return e ? atoi(e) : dflt;
-}
-
-enum Variant { V_SINGLE = 0, V_PAIR = 1, V_PAIR_XSTAT = 2, V_EXPAND = 3, V_EXPAND_XSTAT = 4, V_SPARSE = 5, V_MC2 = 6,
-               V_MC4 = 7, V_PAIR256 = 8 };
-
-// clusters of 2*XM CTAs that can be resident at once (persistent grid size)
-template <typename K>
-int max_clusters(K kern, int cluster, int threads, int smem, int fallback)
-{
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = cluster;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(cluster * 64, 1, 1);
-    cfg.blockDim = dim3(threads, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, (void *)kern, &cfg) != cudaSuccess || n <= 0) {
-        cudaGetLastError();
-        return fallback;
-    }
-    return n;
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const std::pair<const void *, int> key((const void *)kern, dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.insert(key).second) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
 int pick_mgroups(int mtiles, int ntiles, int npairs)

@@ -3,6 +3,7 @@
 #include <stdint.h>
 #include <string>
 
+#include "../../include/sparseinfer_b200.h"
 #include "image.h"
 
 void si_set_error(const std::string &msg);
@@ -36,10 +37,6 @@ bool k2_supported(const SiImage *h, int64_t n, int32_t layout, const void *x, in
 uint64_t k2_workspace(const SiImage *h, int64_t n, int32_t layout);
 int k2_launch_count(const SiImage *h, int32_t layout);
 
-// K2t: X-stationary 2:4 sparse tensor-core kernel (spmm_tcx.cu), token-major X, K <= 1024
-int k2t_launch(const SpmmArgs &a);
-bool k2t_supported(const SiImage *h, int64_t n, int32_t layout, const void *x, int64_t ldx);
-
-// K2a: weight-stationary tensor-core kernel with W in TMEM (spmm_tca.cu), K <= 1024
-int k2a_launch(const SpmmArgs &a);
-bool k2a_supported(const SiImage *h, int64_t n, int32_t layout, const void *x, int64_t ldx);
+// K3: X-stationary 2:4-sparse tensor-core kernel (spmm_xs.cu): token-major X, K <= 1024
+int k3_launch(const SpmmArgs &a);
+bool k3_supported(const SiImage *h, int64_t n, int32_t layout, const void *x, int64_t ldx);

@@ -375,7 +375,7 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
 // the warp never diverges: issued from a divergent lone thread, every tcgen05 /
 // TMA instruction is wrapped by ptxas in an ELECT / BRA.U.ANY loop with
 // R2UR conversions, which made the issue path of a 2:4 stage several times
-// longer than its MMAs (K2t role timelines, tools/k2t_trace.py).
+// longer than its MMAs (K2t role timelines, round 1).
 namespace tcw {
 __device__ __forceinline__ void mma_sp_i8_2sm(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t e_tmem,
                                               uint32_t idesc, uint32_t accum)
@@ -405,6 +405,17 @@ __device__ __forceinline__ void tmem_cp_128x128b_2sm(uint32_t taddr, uint64_t sd
         "{\n\t.reg .pred p;\n\t.reg .b32 r;\n\t"
         "elect.sync r|p, 0xffffffff;\n\t"
         "@p tcgen05.cp.cta_group::2.128x128b [%0], %1;\n}" ::"r"(taddr), "l"(sdesc)
+        : "memory");
+}
+// smem [128 rows x 32 B] (two 16-byte core-matrix columns LBO apart) -> TMEM
+// (128 lanes x 8 columns) in both CTAs of the pair: both metadata tiles of a
+// 128-k 2:4 stage in one instruction
+__device__ __forceinline__ void tmem_cp_128x256b_2sm(uint32_t taddr, uint64_t sdesc)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 r;\n\t"
+        "elect.sync r|p, 0xffffffff;\n\t"
+        "@p tcgen05.cp.cta_group::2.128x256b [%0], %1;\n}" ::"r"(taddr), "l"(sdesc)
         : "memory");
 }
 __device__ __forceinline__ void mma_commit_2sm_mc(uint64_t *bar, uint16_t cta_mask)

@@ -257,25 +257,53 @@ def _run(plan: SpmmPlan, x: torch.Tensor, layout: str, n: int, ldx: int, sides, 
 
 
 def spmm_exec(plan: SpmmPlan, act: ActivationLayout, pool=None, sides=None, out=None,
-              kernel: str = "auto") -> torch.Tensor:
-    """Run the fused SpMM on the GPU (spmm.py:283-333); returns [N, M] CUDA.
+              kernel: str = "auto"):
+    """Run the fused SpMM on the GPU (spmm.py:283-333).
 
-    ``kernel`` selects "auto", "gather" (K1), "tc" (K2) or "ref"."""
+    Returns a CUDA tensor [N, M].  ``out`` may be a CUDA tensor (written in
+    place) or, as in the reference, a host array (numpy / CPU tensor) of shape
+    [N, M] and the program's dtype: the result is computed on the GPU and
+    copied into it, and ``out`` itself is returned.  ``kernel`` selects
+    "auto", "gather" (K1), "tc" (K2) or "ref"."""
     sw = plan.weight
     if act.k != sw.cols or act.n != plan.n or act.bn != plan.bn:
         raise ValueError("activation layout does not match the plan")
+    host_out = out is not None and not (isinstance(out, torch.Tensor) and out.is_cuda)
+    if host_out:
+        dt = plan.program.out_dtype
+        shape_ok = tuple(out.shape) == (plan.n, sw.logical_rows)
+        dtype_ok = (out.dtype == dt.np) if isinstance(out, np.ndarray) else (out.dtype == _TORCH_DT[dt])
+        if not (shape_ok and dtype_ok):
+            raise ValueError("bad output buffer")
+        res = _run(plan, act.data, act.orient, act.n, act.ld, sides, None, kernel)
+        if isinstance(out, np.ndarray):
+            np.copyto(out, res.cpu().numpy())
+        else:
+            out.copy_(res)
+        return out
     return _run(plan, act.data, act.orient, act.n, act.ld, sides, out, kernel)
 
 
-_HOST_WS: dict = {}
+def _host_sides(sides, n_sides: int, n: int, m: int):
+    """The reference's side check (spmm.py:300-304): a host f32 [n_sides, N, M]
+    stack (pack_sides form), contiguous for the per-chunk copies."""
+    if n_sides == 0:
+        return None
+    if sides is None:
+        raise ValueError(f"program needs {n_sides} side inputs")
+    t = sides if isinstance(sides, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(sides, np.float32))
+    if t.is_cuda:
+        raise ValueError("spmm_exec_host: sides must be host memory")
+    t = t.to(torch.float32).contiguous()
+    if t.ndim != 3 or t.shape[0] < n_sides or t.shape[1] != n or t.shape[2] != m:
+        raise ValueError(f"program needs {n_sides} side inputs")
+    return t
 
 
-def _host_job(plan: SpmmPlan, x, layout: str, out):
+def _host_job(plan: SpmmPlan, x, layout: str, out, sides=None):
     sw = plan.weight
     m = sw.logical_rows
     prog = plan.program
-    if prog.n_sides:
-        raise ValueError("spmm_exec_host: programs with side inputs need spmm_exec")
     xt = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
     if xt.is_cuda or xt.dtype != torch.uint8 or xt.ndim != 2:
         raise ValueError("spmm_exec_host: x must be a host u8 matrix")
@@ -289,34 +317,36 @@ def _host_job(plan: SpmmPlan, x, layout: str, out):
         raise ValueError("activation does not match the plan")
     if xt.stride(1) != 1:
         xt = xt.contiguous()
+    st = _host_sides(sides, prog.n_sides, n, m)
     dt = _TORCH_DT[prog.out_dtype]
     if out is None:
         out = torch.empty((n, m), dtype=dt).pin_memory()
     elif tuple(out.shape) != (n, m) or out.dtype != dt or out.is_cuda or (m > 1 and out.stride(1) != 1):
         raise ValueError("bad output buffer")
     job = _lib.SiHostJob(_lib.ptr(plan.image), plan.image_dev.data_ptr(), xt.data_ptr(), _lib.LAYOUTS[layout],
-                         _ld(xt), n, out.data_ptr(), _ld(out))
-    return job, xt, out
+                         _ld(xt), n, out.data_ptr(), _ld(out), st.data_ptr() if st is not None else None)
+    return job, (xt, st), out
 
 
 def spmm_exec_host_batch(items, chunk: int = 8192, kernel: str = "auto") -> list:
     """Several independent spmm_exec calls on host buffers as one pipelined
     chunk sequence (si_spmm_host_batch): ``items`` is a list of
-    (plan, x, layout, out) with out None for a new pinned tensor.  The
-    copy-in of one job overlaps the copy-out of the previous one."""
+    (plan, x, layout, out) or (plan, x, layout, out, sides) with out None for
+    a new pinned tensor and sides the host f32 [n_sides, N, M] stack.  The
+    copy-in of one job overlaps the copy-out of the previous one.
+
+    Reentrant: every call sizes and allocates its own device workspace (from
+    the caching allocator, on the current stream) and the library gives it a
+    private pair of copy streams, so threads may call concurrently."""
     L = _lib.lib()
     if not items:
         return []
-    built = [_host_job(p, x, lay, o) for (p, x, lay, o) in items]
+    built = [_host_job(*it) for it in items]
     jobs = (_lib.SiHostJob * len(built))(*[b[0] for b in built])
     dev = items[0][0].image_dev.device
     need = ctypes.c_uint64(0)
     _lib.check(L.si_spmm_host_batch_workspace_size(jobs, len(built), chunk, ctypes.byref(need)), "spmm_exec_host")
-    key = (dev.index, int(need.value))
-    ws = _HOST_WS.get(key)
-    if ws is None:
-        _HOST_WS.clear()
-        ws = _HOST_WS[key] = torch.empty(int(need.value), dtype=torch.uint8, device=dev)
+    ws = torch.empty(int(need.value), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev).cuda_stream
     rc = L.si_spmm_host_batch(jobs, len(built), ws.data_ptr(), need.value, chunk, _lib.KERNELS[kernel], stream)
     _lib.check(rc, "spmm_exec_host")
@@ -324,14 +354,15 @@ def spmm_exec_host_batch(items, chunk: int = 8192, kernel: str = "auto") -> list
 
 
 def spmm_exec_host(plan: SpmmPlan, x, layout: str = "kn", out=None, chunk: int = 8192,
-                   kernel: str = "auto") -> torch.Tensor:
+                   kernel: str = "auto", sides=None) -> torch.Tensor:
     """spmm_exec on host buffers (the reference's call takes host arrays,
     spmm.py:283-333): ``x`` is the logical [K, N] (layout "kn") or token-major
-    [N, K] ("nk") u8 activation in host memory, the result [N, M] comes back
-    in host memory (``out`` or a new pinned tensor).  Token chunks are
-    pipelined by the library (si_spmm_host): copy-in, kernel and copy-out of
-    neighbouring chunks overlap.  Pinned inputs give full overlap."""
-    return spmm_exec_host_batch([(plan, x, layout, out)], chunk=chunk, kernel=kernel)[0]
+    [N, K] ("nk") u8 activation in host memory, ``sides`` the host f32
+    [n_sides, N, M] residual stack the program needs, and the result [N, M]
+    comes back in host memory (``out`` or a new pinned tensor).  Token chunks
+    are pipelined by the library (si_spmm_host): copy-in, kernel and copy-out
+    of neighbouring chunks overlap.  Pinned inputs give full overlap."""
+    return spmm_exec_host_batch([(plan, x, layout, out, sides)], chunk=chunk, kernel=kernel)[0]
 
 
 def spmm_ref(sw: Sparse4x1Weight, a, program: EpilogueProgram | None = None, bias=None,

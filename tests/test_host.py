@@ -151,7 +151,31 @@ def test_native_library_exports_every_header_symbol():
     assert "si_spmm" in syms and "si_plan_image_build" in syms
     for s in syms:
         assert hasattr(L, s), s
-    assert _lib.lib().si_abi_version() == 1
+    assert _lib.lib().si_abi_version() == _lib.ABI_VERSION
+
+
+def test_host_workspace_queries_agree():
+    """si_spmm_host_workspace_size (the single-job query INTEGRATION.md
+    documents) sizes exactly what si_spmm_host_batch needs for that job, with
+    and without side inputs (no GPU needed: pure host-side layout)."""
+    from paper_2306_16601_b200.kernels.spmm import _build_image
+    from paper_2306_16601_b200 import workloads
+    L = _lib.lib()
+    w, _, bias, scales = workloads.baseline_inputs(1024, 768, 1, 0.9, 5, with_x=False)
+    from paper_2306_16601_b200 import kernels as K
+    sw = P.encode_sparse(w, scales)
+    for prog in (workloads.program("requant_u8", scales),
+                 K.build_program(scales, 1.0, 0, None, [("dequantize_acc",), ("add_side", 0)])):
+        img, _ = _build_image(sw, prog, bias)
+        for lay in (0, 1):
+            for chunk in (1, 1000, 4096, 32768):
+                one = ctypes.c_uint64(0)
+                assert L.si_spmm_host_workspace_size(_lib.ptr(img), chunk, lay, 0, ctypes.byref(one)) == 0
+                dummy = ctypes.c_void_p(16)
+                job = _lib.SiHostJob(_lib.ptr(img), dummy, dummy, lay, 1 << 20, 1 << 20, dummy, 4096, dummy)
+                batch = ctypes.c_uint64(0)
+                assert L.si_spmm_host_batch_workspace_size(ctypes.byref(job), 1, chunk, ctypes.byref(batch)) == 0
+                assert one.value == batch.value > 0, (lay, chunk)
 
 
 def test_native_library_is_sm100a_only():
