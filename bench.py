@@ -234,10 +234,12 @@ def main():
     ap.add_argument("--e2e-chunk", type=int, default=32768, help="token chunk of the host pipeline")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the config-3 / config-1 cells")
     ap.add_argument("--shard", default="tokens", choices=["tokens", "rows"],
                     help="tokens: each rank its own 65536 tokens, no collective (weak scaling); rows: the weight "
-                         "rows of every linear split over the ranks, one NCCL all-gather of the u8 outputs per "
-                         "linear (strong scaling, SURVEY 8(e))")
+                         "rows of every linear split over the ranks, each rank's block written in place and pushed "
+                         "into its peers' outputs (symmetric memory; NCCL all-gather where peers cannot be mapped) "
+                         "(strong scaling, SURVEY 8(e))")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return relaunch_distributed(sys.argv[1:], args.gpus)
@@ -388,6 +390,39 @@ def main():
     # (rows mode: the host-buffer path runs each rank's full linears unsharded)
     e2e_value = ops_step * world / (float(te.item()) / 1e3) / 1e12
 
+    # ---- secondary cells (not the metric): BASELINE config 3 (fused FFN-up,
+    # erf GELU -> u8, N = 4096) and config 1 (768^2, N = 128), device-timed
+    # with CUDA-graph replay; inputs 3-16 MB are L2-resident across replays
+    secondary = {}
+    if not rows_mode and not args.no_secondary:
+        for c in (workloads.CONFIG3, workloads.CONFIG1[1]):
+            w, x, bias, scales = workloads.baseline_inputs(c.m, c.k, c.n, c.ratio, c.seed)
+            sw = P.encode_sparse(w, scales)
+            plan = K.plan_spmm(sw, c.n, program=workloads.program(c.program, scales), bias=bias, device=dev)
+            act = K.relayout_activation(torch.from_numpy(x).pin_memory(), device=dev)
+            from paper_2306_16601_b200.kernels.spmm import _TORCH_DT
+            o = torch.empty((c.n, c.m), dtype=_TORCH_DT[plan.program.out_dtype], device=dev)
+            for _ in range(3):
+                K.spmm_exec(plan, act, out=o)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for _ in range(20):
+                    K.spmm_exec(plan, act, out=o)
+            g.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) / 20 * 1e3
+            gbs = c.hbm_bytes() / (us / 1e6) / 1e9
+            secondary[c.name] = {"us_per_call": round(us, 2), "tops": round(c.ops() / (us / 1e6) / 1e12, 1),
+                                 "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": peak,
+                                              "unit": "GB/s", "frac": round(gbs / peak, 4),
+                                              "algorithmic_bytes": c.hbm_bytes()},
+                                 "timing": "CUDA graph of 20 back-to-back calls, L2-warm"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(cells, budget_s=args.cpu_budget)
@@ -404,7 +439,7 @@ def main():
                        "activation_layout": ("token-major [N, K] (relayout_tokens)" if args.layout == "nk"
                                              else "[K, N] (relayout_activation)"),
                        "l2": "no flush: each step touches ~768 MB >> 126 MB L2",
-                       "parallelism": (f"row-shard x{world} + NCCL all-gather of the u8 outputs" if rows_mode
+                       "parallelism": (f"row-shard x{world} + peer exchange of the u8 outputs" if rows_mode
                                        else f"token-shard x{world} (no collective)"),
                        "launch": "eager" if args.no_graphs else "CUDA graph per linear (replay)"},
             "gpu_launches": launches_per_step * args.steps,
@@ -419,6 +454,7 @@ def main():
                             f"{args.e2e_chunk}-token chunks pipelined (H2D / kernel / D2H)"},
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "secondary": secondary,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -41,7 +41,10 @@ constexpr int STG_BYTES = EPI_GROUPS * STG_GROUP;
 constexpr int TABLE_BYTES = 16 * 1024;      // breakpoint tables staged in smem (EPI_DEQ_TABLE)
 constexpr int SMEM_MAX = 232448;
 
-enum OutKind { OUT_32 = 0, OUT_U8_TMA = 1, OUT_S8_TMA = 2, OUT_8_DIRECT = 3 };
+// 8-bit outputs: *_TMA stage a 128-row group tile (swizzled, one TMA store
+// per column group), *_W a per-warp 32-row tile (row-major 32 B, one TMA
+// store per warp and chunk, no cross-warp barrier)
+enum OutKind { OUT_32 = 0, OUT_U8_TMA = 1, OUT_S8_TMA = 2, OUT_8_DIRECT = 3, OUT_U8_W = 4, OUT_S8_W = 5 };
 
 struct K2Params {
     int32_t mtiles;      // weight-row tiles (128 rows single-CTA, 256 rows per pair)
@@ -279,6 +282,20 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, i
 #pragma unroll
             for (int j = 0; j < 32; ++j)
                 if (n0 + j < P.N) reinterpret_cast<uint8_t *>(P.out)[(n0 + j) * P.ldo + m] = (uint8_t)(v[j] & 0xFF);
+        }
+    } else if constexpr (OUTK == OUT_U8_W || OUTK == OUT_S8_W) {
+        // saturating pack of 4 consecutive tokens, quad transpose to 4
+        // consecutive m, STS into this warp's [32 token][32 m] tile: the
+        // lanes of one store cover 4 token rows x 32 bytes (conflict-free)
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            uint32_t word;
+            if (OUTK == OUT_U8_W)
+                word = tc::pack_sat_u8(v[4 * w + 1], v[4 * w], tc::pack_sat_u8(v[4 * w + 3], v[4 * w + 2], 0));
+            else
+                word = tc::pack_sat_s8(v[4 * w + 1], v[4 * w], tc::pack_sat_s8(v[4 * w + 3], v[4 * w + 2], 0));
+            word = quad_transpose(word, W.selA, W.selB);
+            *reinterpret_cast<uint32_t *>(W.stg + (4 * w + W.u) * 32 + 4 * W.i4) = word;
         }
     } else {
         // saturating pack of 4 consecutive tokens, quad transpose to 4

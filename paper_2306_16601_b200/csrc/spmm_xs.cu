@@ -25,13 +25,17 @@
 //    one tcgen05.cp (both metadata tiles, 128x256b) + two MMAs with
 //    descriptors formed by adding offsets to precomputed bases.
 //
-// Roles (20 warps): warps 0, 14 and 19 TMA producers (stage i on producer
-// i mod 3), warp 1 TMEM allocator + MMA issuer (leader CTA), warps 2-13 the
-// epilogue (3 token-column groups x 4 TMEM lane quarters; the compiled
-// _run_chain forms of k2_common.cuh), warps 15-18 the residual gather (the
-// first also forwards this CTA's X-chunk arrivals to the leader).  TMEM: two 224-column
+// Roles (20 warps, 96 registers each): warps 0, 14 and 19 TMA producers
+// (stage i on producer i mod 3), warp 1 TMEM allocator + MMA issuer (leader
+// CTA), warps 2-13 the epilogue (3 token-column groups x 4 TMEM lane
+// quarters; the compiled _run_chain forms of k2_common.cuh), warps 15-18 the
+// residual gather (the first also forwards this CTA's X-chunk arrivals to
+// the leader).  8-bit outputs leave per warp: each warp stages its own 32
+// rows x 32 tokens (1 KB, no cross-warp barrier) and TMA-stores them.  TMEM: two 224-column
 // accumulators (the epilogue of tile i overlaps the MMAs of tile i+1) + two
 // 8-column metadata slots.
+#include <cstdio>
+
 #include "k2_common.cuh"
 
 namespace {
@@ -67,15 +71,15 @@ constexpr int XS_PROD1_WARP = 2 + XS_EPI_WARPS;      // 14
 constexpr int XS_GATHER_WARP = XS_PROD1_WARP + 1;    // 15 .. 18
 constexpr int XS_NGATHER = 4;
 constexpr int XS_PROD2_WARP = XS_GATHER_WARP + XS_NGATHER;   // 19
-constexpr int XS_THREADS = 32 * (XS_PROD2_WARP + 1);
-constexpr int XS_STG = 128 * 32;                     // 8-bit staging slot: 128 m x 32 tokens
+constexpr int XS_THREADS = 32 * (XS_PROD2_WARP + 1);         // 20 warps: 96 registers each
+constexpr int XS_WSTG = 32 * 32;                     // 8-bit staging slot of one warp: 32 tokens x 32 m
 constexpr int XS_MAXPAIRS = 512;                     // residual MMA counts staged in smem (M <= 131072)
 constexpr uint32_t XS_ECOL = 2 * XS_TN;              // metadata slots: TMEM columns 448..463
 static_assert(XS_ECOL + 16 <= 512, "TMEM budget");
 static_assert(XS_TNH % 8 == 0, "token half must keep whole 8-row SW128 atoms");
 
 template <int OUTK>
-constexpr int xs_staged() { return (OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA) ? 2 * XS_EPI_GROUPS * XS_STG : 0; }
+constexpr int xs_staged() { return (OUTK == OUT_U8_W || OUTK == OUT_S8_W) ? XS_EPI_WARPS * XS_WSTG : 0; }
 template <int MODE, int OUTK>
 constexpr int xs_fixed()
 {
@@ -99,7 +103,23 @@ struct XsParams {
     const uint16_t *tr_k;    // [ptiles][TR_SLOTS] activation column per residual slot
     const int32_t *tr_cnt;   // [ptiles] residual MMAs (64 slots each)
     int32_t exp;             // experiment switches (XsExp; experiment builds only)
+    unsigned long long *trace;   // experiment builds: pair 0's role timelines, else null
 };
+
+// experiment builds only: (event << 56 | globaltimer ns) per role of pair 0
+#ifdef SI_EXPERIMENTS
+constexpr int XS_TRACE_N = 4096;
+__device__ __forceinline__ void xs_trace(const XsParams &X, int role, int &cnt, unsigned ev)
+{
+    if (!X.trace || cnt >= XS_TRACE_N || (blockIdx.x >> 1) != 0) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    X.trace[role * XS_TRACE_N + cnt++] = ((unsigned long long)ev << 56) | (t & 0x00FFFFFFFFFFFFFFull);
+}
+#define XS_TRACE(role, cnt, ev) xs_trace(X, role, cnt, ev)
+#else
+#define XS_TRACE(role, cnt, ev) ((void)0)
+#endif
 
 // per-row epilogue constants of one accumulator tile, loaded a tile ahead
 struct XsRow {
@@ -121,14 +141,14 @@ __device__ __forceinline__ XsRow xs_row(int32_t m, const K2Params &P, const EpiP
 }
 
 // Epilogue of one accumulator for one warp: its 32 rows x the column group's
-// 32-token chunks (g, g+3, g+6), each staged and TMA-stored from one of two
-// alternating slots (a slot is rewritten once the store issued from it two
-// chunks earlier has read it).  The accumulator is released once this warp's
-// last chunk is in registers.
+// 32-token chunks (g, g+3, g+6), each staged in this warp's own 1 KB tile and
+// TMA-stored by its lane 0 (the tile is rewritten once that store has read
+// it).  The accumulator is released once this warp's last chunk is in
+// registers.
 template <int MODE, int OUTK, typename Release>
 __device__ __forceinline__ void xs_epi_tile(uint32_t lane_base, int32_t row0, int64_t tok0,
                                             const CUtensorMap *tmap_o, const K2Params &P, const EpiParams &E,
-                                            EpiWarp &W, const XsRow &k, int &slot, Release release,
+                                            EpiWarp &W, const XsRow &k, Release release,
                                             const XsParams &X)
 {
     if (XS_EXP(XE_NO_EPI)) {
@@ -137,7 +157,7 @@ __device__ __forceinline__ void xs_epi_tile(uint32_t lane_base, int32_t row0, in
         if (W.lane == 0) release();
         return;
     }
-    constexpr bool STAGED = (OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA);
+    constexpr bool STAGED = (OUTK == OUT_U8_W || OUTK == OUT_S8_W);
     const int32_t m = row0 + W.q * 32 + W.lane;
     const bool mok = m < E.M;
     const bool proven = __all_sync(0xffffffffu, k.gr >= 1.0f);
@@ -145,7 +165,6 @@ __device__ __forceinline__ void xs_epi_tile(uint32_t lane_base, int32_t row0, in
     const bool fast = !wide && __all_sync(0xffffffffu, k.gr >= 0.0f);
     const float gm = proven ? (wide ? 2.0f : 1.0f) : (k.gr >= 1.0f ? 0.0f : fmaxf(k.gr, 0.0f));
     const float cq = proven ? k.cp : k.cq;
-    uint8_t *const stg0 = W.stg;
     auto rel = [&]() {
         tc::tc_fence_before();
         __syncwarp();
@@ -155,9 +174,9 @@ __device__ __forceinline__ void xs_epi_tile(uint32_t lane_base, int32_t row0, in
     for (int ch = W.g; ch < XS_NCH; ch += XS_EPI_GROUPS) {
         const bool last = ch + XS_EPI_GROUPS >= XS_NCH;
         if constexpr (STAGED) {
-            if (W.q == 2 && W.lane == 0) tc::tma_store_wait_read1();
-            tc::named_bar_sync(1 + W.g, 128);
-            W.stg = stg0 + slot * XS_STG;
+            // this warp's previous store must have read its staging tile
+            if (W.lane == 0) tc::tma_store_wait_read0();
+            __syncwarp();
         }
         if (last)
             epi_chunk<MODE, OUTK>(lane_base + ch * 32, m, mok, k.adj, k.s_in, cq, gm, fast, tok0 + ch * 32, 0, P, E,
@@ -167,15 +186,13 @@ __device__ __forceinline__ void xs_epi_tile(uint32_t lane_base, int32_t row0, in
                                   W);
         if constexpr (STAGED) {
             tc::fence_proxy_async_smem();
-            tc::named_bar_sync(1 + W.g, 128);
-            if (W.q == 2 && W.lane == 0 && !XS_EXP(XE_NO_STORE)) {
-                tc::tma_store_2d(tmap_o, W.stg, row0, (int32_t)(tok0 + ch * 32));
+            __syncwarp();
+            if (W.lane == 0 && !XS_EXP(XE_NO_STORE)) {
+                tc::tma_store_2d(tmap_o, W.stg, row0 + W.q * 32, (int32_t)(tok0 + ch * 32));
                 tc::tma_store_commit();
             }
-            slot ^= 1;
         }
     }
-    W.stg = stg0;
 }
 
 template <int MODE, int OUTK>
@@ -298,7 +315,7 @@ k3_kernel(const __grid_constant__ CUtensorMap tmap_s, const __grid_constant__ CU
             const uint64_t edesc0 = tc::smem_desc(ring_u + 8192, 2048, 128, 0);
             const uint64_t bdesc0 = tc::smem_desc_sw128(tc::smem_u32(xbuf), 16, 1024);
             const uint64_t rdesc0 = tc::smem_desc_sw128(tc::smem_u32(rbuf), 16, 1024);
-            int stage = 0, acc = 0;
+            int stage = 0, acc = 0, tcnt = 0;
             uint32_t phase = 0, acc_phase = 0, xphase = 0, rphase = 0, eslot = 0;
             for (int unit = pair; unit < units; unit += npairs) {
                 int nt, p_lo, p_hi;
@@ -307,6 +324,7 @@ k3_kernel(const __grid_constant__ CUtensorMap tmap_s, const __grid_constant__ CU
                     const int pt = pair_tile(p_lo, p_hi, i);
                     const int nres = s_rcnt[pt];
                     tc::mbar_spin(&tempty[acc], acc_phase ^ 1);
+                    if (lane == 0) XS_TRACE(0, tcnt, 1);
                     tc::tc_fence_after();
                     const uint32_t d_tmem = tmem_base + acc * XS_TN;
                     for (int kc = 0; kc < X.kchunks; ++kc) {
@@ -314,7 +332,9 @@ k3_kernel(const __grid_constant__ CUtensorMap tmap_s, const __grid_constant__ CU
                             tc::mbar_spin(&xfull[kc], xphase);
                             tc::mbar_spin_cluster(&xpeer[kc], xphase);
                         }
+                        if (lane == 0) XS_TRACE(0, tcnt, 10);
                         tc::mbar_spin(&full[stage], phase);
+                        if (lane == 0) XS_TRACE(0, tcnt, 2);
                         tc::tc_fence_after();
                         const uint64_t so = (uint64_t)((stage * XS_IMG) >> 4);
                         const uint32_t e_tmem = tmem_base + XS_ECOL + 8 * eslot;
@@ -333,6 +353,7 @@ k3_kernel(const __grid_constant__ CUtensorMap tmap_s, const __grid_constant__ CU
                         // residual slots: B from the gathered buffers of both CTAs
                         tc::mbar_spin(&full[stage], phase);
                         tc::mbar_spin_cluster(rfull, rphase);
+                        if (lane == 0) XS_TRACE(0, tcnt, 3);
                         tc::tc_fence_after();
                         const uint64_t so = (uint64_t)((stage * XS_IMG) >> 4);
                         const uint32_t e_tmem = tmem_base + XS_ECOL + 8 * eslot;
@@ -349,6 +370,7 @@ k3_kernel(const __grid_constant__ CUtensorMap tmap_s, const __grid_constant__ CU
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                     tcw::mma_commit_2sm_mc(&tfull[acc], 0x3);
+                    if (lane == 0) XS_TRACE(0, tcnt, 4);
                     acc ^= 1;
                     if (acc == 0) acc_phase ^= 1;
                 }
@@ -361,6 +383,7 @@ k3_kernel(const __grid_constant__ CUtensorMap tmap_s, const __grid_constant__ CU
         // the resident SW128 X tile into the same layout; forwards this CTA's
         // X-chunk arrivals to the leader (its MMA cannot wait on a peer barrier)
         const int gi = warp - XS_GATHER_WARP;
+        int tcnt = 0;
         const uint32_t rfull0 = tc::mapa(tc::smem_u32(rfull), 0);
         const uint32_t xpeer0 = tc::mapa(tc::smem_u32(xpeer), 0);
         uint32_t xphase = 0, rphase = 0;
@@ -384,6 +407,7 @@ k3_kernel(const __grid_constant__ CUtensorMap tmap_s, const __grid_constant__ CU
 #pragma unroll
                 for (int b = 0; b < 4; ++b) kk4[b] = __ldg(kp + b);
                 tc::mbar_wait(rempty, rphase ^ 1);
+                if (lane == 0 && rank == 0) XS_TRACE(13 + gi, tcnt, 8);
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
                     kofs[b] = (kk4[b] >> 7) * XS_XCH + (kk4[b] & 15);
@@ -402,6 +426,7 @@ k3_kernel(const __grid_constant__ CUtensorMap tmap_s, const __grid_constant__ CU
                 tc::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive_cluster(rfull0);
+                if (lane == 0 && rank == 0) XS_TRACE(13 + gi, tcnt, 9);
                 rphase ^= 1;
             }
             // every read of this unit's X tile is done: second arrival on the chunks
@@ -413,11 +438,11 @@ k3_kernel(const __grid_constant__ CUtensorMap tmap_s, const __grid_constant__ CU
     } else {
         // ---------------- epilogue warps (both CTAs; each reads its own TMEM half)
         EpiWarp W = make_epi_warp<MODE, XS_EPI_WARPS>(warp, lane, staging, tables, E);
-        W.stg = staging + W.g * (2 * XS_STG);
+        W.stg = staging + (warp - 2) * XS_WSTG;
         const uint32_t tempty0 = tc::mapa(tc::smem_u32(tempty), 0);
         const int32_t mrow = 128 * (int)rank + W.q * 32 + lane;   // this lane's row within a pair tile
         const uint32_t lane_off = (uint32_t)(W.q * 32) << 16;
-        int acc = 0, slot = 0;
+        int acc = 0, tcnt = 0;
         uint32_t acc_phase = 0;
         for (int unit = pair; unit < units; unit += npairs) {
             int nt, p_lo, p_hi;
@@ -427,16 +452,19 @@ k3_kernel(const __grid_constant__ CUtensorMap tmap_s, const __grid_constant__ CU
                 // row constants: loads issued before blocking on the accumulator
                 const XsRow k = xs_row<MODE>(pt * 256 + mrow, P, E);
                 const uint32_t te = tempty0 + 8 * acc;
+                const int role = 1 + (warp - 2);
                 tc::mbar_wait(&tfull[acc], acc_phase);
+                if (lane == 0 && rank == 0) XS_TRACE(role, tcnt, 5);
                 tc::tc_fence_after();
                 xs_epi_tile<MODE, OUTK>(tmem_base + lane_off + acc * XS_TN, pt * 256 + 128 * (int)rank,
-                                        (int64_t)nt * XS_TN, &tmap_o, P, E, W, k, slot,
-                                        [&, te] { tc::mbar_arrive_cluster(te); }, X);
+                                        (int64_t)nt * XS_TN, &tmap_o, P, E, W, k,
+                                        [&, te] { tc::mbar_arrive_cluster(te); if (rank == 0) XS_TRACE(role, tcnt, 6); }, X);
+                if (lane == 0 && rank == 0) XS_TRACE(role, tcnt, 7);
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;
             }
         }
-        if ((OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA) && W.q == 2 && lane == 0) tc::tma_store_wait_all0();
+        if ((OUTK == OUT_U8_W || OUTK == OUT_S8_W) && lane == 0) tc::tma_store_wait_all0();
     }
     tc::tc_fence_before();
     tc::cluster_sync();
@@ -517,19 +545,42 @@ int k3_launch(const SpmmArgs &a)
     X.tr_k = img_sec<uint16_t>(a.img, h->off_tr_k);
     X.tr_cnt = img_sec<int32_t>(a.img, h->off_tr_cnt);
     X.exp = 0;
+    X.trace = nullptr;
 #ifdef SI_EXPERIMENTS
     if (const char *e = getenv("SI_XS_EXP")) X.exp = atoi(e);
+    static unsigned long long *trace_buf = nullptr;
+    const char *trace_path = getenv("SI_XS_TRACE");
+    const size_t trace_bytes = (size_t)20 * XS_TRACE_N * 8;
+    if (trace_path) {
+        if (!trace_buf) cudaMalloc(&trace_buf, trace_bytes);
+        cudaMemsetAsync(trace_buf, 0, trace_bytes, (cudaStream_t)a.stream);
+        X.trace = trace_buf;
+    }
+    // (the launch below; then, tracing: wait for it and write the timeline)
+    struct Dump {
+        const char *path; unsigned long long *buf; size_t bytes; cudaStream_t st;
+        ~Dump()
+        {
+            if (!path || !buf) return;
+            std::string hb(bytes, '\0');
+            cudaStreamSynchronize(st);
+            cudaMemcpy(&hb[0], buf, bytes, cudaMemcpyDeviceToHost);
+            if (FILE *f = fopen(path, "wb")) { fwrite(hb.data(), 1, bytes, f); fclose(f); }
+        }
+    } dump{trace_path, trace_buf, trace_bytes, (cudaStream_t)a.stream};
 #endif
     if (h->out_dtype == SI_F32 || h->out_dtype == SI_S32) {
         std::memset(&to, 0, sizeof(to));
         return k3_launch_outk<OUT_32>(a, ts, tr, tx, to, p, X);
     }
+    // 8-bit outputs: per-warp boxes of 32 rows x 32 tokens
     const bool tma_ok = (a.ldo % 16 == 0) && ((uintptr_t)a.out % 16 == 0) &&
-                        encode_2d(&to, a.out, (uint64_t)h->M, (uint64_t)a.n, (uint64_t)a.ldo, 128, 32);
+                        encode_2d(&to, a.out, (uint64_t)h->M, (uint64_t)a.n, (uint64_t)a.ldo, 32, 32,
+                                  CU_TENSOR_MAP_SWIZZLE_NONE);
     if (!tma_ok) {
         std::memset(&to, 0, sizeof(to));
         return k3_launch_outk<OUT_8_DIRECT>(a, ts, tr, tx, to, p, X);
     }
-    return h->out_dtype == SI_U8 ? k3_launch_outk<OUT_U8_TMA>(a, ts, tr, tx, to, p, X)
-                                 : k3_launch_outk<OUT_S8_TMA>(a, ts, tr, tx, to, p, X);
+    return h->out_dtype == SI_U8 ? k3_launch_outk<OUT_U8_W>(a, ts, tr, tx, to, p, X)
+                                 : k3_launch_outk<OUT_S8_W>(a, ts, tr, tx, to, p, X);
 }

@@ -12,16 +12,22 @@ The two multi-GPU modes are those two axes:
   answer.  Weak or strong scaling depending on whether N grows with ranks.
 * ``rows`` -- M-sharding with one exchange step.  Each rank owns a
   contiguous range of whole 4-row groups, reads the full activation and
-  produces out[:, m0:m1].  The shards are exchanged with an NCCL
-  all-gather; because a rank's block is a column slice of [N, M], the
-  gathered [world, N, Mr] buffer is re-laid into [N, M] with one copy.
-  (The single-GPU builds used here cannot exercise a peer-store variant;
-  si_spmm already accepts (out + m0, ldo = M) so a rank can write its slice
-  straight into a peer-mapped [N, M] buffer when one is available.)
+  produces out[:, m0:m1].  The kernel writes that block straight into the
+  rank's final [N, M] output (si_spmm takes out + m0 with ldo = M), so the
+  local block is never copied.  Exchange:
+    - ``symm`` (NCCL groups whose GPUs can map each other's memory): the
+      output lives in torch symmetric memory and every rank pushes its block
+      into the same columns of each peer's buffer over NVLink (strided peer
+      copies), then a barrier -- the result lands in final layout on every
+      rank, with no gathered intermediate and no re-layout pass;
+    - ``gather`` (gloo / no peer mapping): one all-gather of equal-size
+      blocks into [world, N, Mr], then the peer blocks are written into the
+      final buffer's columns.
 
-Everything here is host bookkeeping around the product's SpMM; the
-gloo-backed CPU tests (tests/test_parallel_gloo.py) check the bookkeeping
-with the oracle standing in for the per-rank compute.
+Everything here is host bookkeeping around the product's SpMM; the per-rank
+compute is injectable, so the gloo-backed CPU tests
+(tests/test_parallel_gloo.py) run RowShardedSpmm itself with the oracle as
+the compute.
 """
 
 from __future__ import annotations
@@ -86,26 +92,44 @@ def shard_program(prog: EpilogueProgram, m0: int, m1: int) -> EpilogueProgram:
                            n_sides=prog.n_sides)
 
 
-def assemble_rows(gathered, n: int, m: int, world: int, rows_pad: int, bounds):
-    """[world, N, rows_pad] gathered shards -> [N, M] (torch or numpy)."""
-    parts = [gathered[r, :, : bounds[r][1] - bounds[r][0]] for r in range(world)]
+def assemble_rows(gathered, n: int, m: int, world: int, rows_pad: int, bounds, out=None, skip: int = -1):
+    """[world, N, rows_pad] gathered blocks -> columns of the [N, M] result
+    (torch or numpy).  ``out`` is written in place when given (its block
+    ``skip`` is left as it is: the rank's own block is already there)."""
     try:
         import torch
-        if isinstance(gathered, torch.Tensor):
-            return torch.cat(parts, dim=1)
+        is_torch = isinstance(gathered, torch.Tensor)
     except ImportError:  # pragma: no cover
-        pass
-    return np.concatenate(parts, axis=1)
+        is_torch = False
+    if out is None:
+        if is_torch:
+            out = torch.empty((n, m), dtype=gathered.dtype, device=gathered.device)
+        else:
+            out = np.empty((n, m), dtype=gathered.dtype)
+    for r in range(world):
+        m0, m1 = bounds[r]
+        if r != skip and m1 > m0:
+            out[:, m0:m1] = gathered[r, :, : m1 - m0]
+    return out
+
+
+def _product_compute(plan, act, out, kernel):
+    from .kernels import spmm as K
+    K.spmm_exec(plan, act, out=out, kernel=kernel)
 
 
 class RowShardedSpmm:
     """M-sharded SpMM over a torch.distributed group (NCCL on GPUs).
 
-    ``run(act)`` computes this rank's [N, Mr] slice with the product kernel,
-    all-gathers the slices and returns the full [N, M] on every rank."""
+    ``run(act)`` computes this rank's block of rows with the product kernel,
+    written straight into the final [N, M] buffer, exchanges the blocks and
+    returns the full [N, M] on every rank.  ``compute(plan, act, out_view,
+    kernel)`` replaces the per-rank SpMM (tests run the bookkeeping on CPU
+    with the oracle); ``exchange`` is "auto" (symm when available), "symm" or
+    "gather"."""
 
     def __init__(self, sw: Sparse4x1Weight, n: int, program: EpilogueProgram, bias=None, group=None,
-                 device=None):
+                 device=None, compute=None, exchange: str = "auto"):
         import torch
         import torch.distributed as dist
 
@@ -120,24 +144,51 @@ class RowShardedSpmm:
         bias = np.zeros(sw.logical_rows, np.int32) if bias is None else np.asarray(bias, np.int32)
         self.plan = K.plan_spmm(mine.weight, n, program=shard_program(program, mine.m0, mine.m1),
                                 bias=bias[mine.m0: mine.m1], device=device)
+        self.compute = compute or _product_compute
         self.rows_pad = mine.rows_pad
-        dt = K._TORCH_DT[program.out_dtype]
-        dev = self.plan.image_dev.device
-        self.local = torch.zeros((n, self.rows_pad), dtype=dt, device=dev)
-        self.gathered = torch.empty((self.world, n, self.rows_pad), dtype=dt, device=dev)
         self.bounds = [(s.m0, s.m1) for s in self.shards]
+        self.dtype = K._TORCH_DT[program.out_dtype]
+        dev = self.plan.image_dev.device
+        self.symm = None
+        if exchange in ("auto", "symm") and dev.type == "cuda" and dist.get_backend(group) == "nccl":
+            try:
+                import torch.distributed._symmetric_memory as symm_mem
+                self.out = symm_mem.empty((n, self.m), dtype=self.dtype, device=dev)
+                self.symm = symm_mem.rendezvous(self.out, group=group or dist.group.WORLD)
+            except Exception:
+                if exchange == "symm":
+                    raise
+                self.symm = None
+        if self.symm is None:
+            self.out = torch.empty((n, self.m), dtype=self.dtype, device=dev)
+            self.local = torch.zeros((n, self.rows_pad), dtype=self.dtype, device=dev)
+            self.gathered = torch.empty((self.world, n, self.rows_pad), dtype=self.dtype, device=dev)
+        self.exchange = "symm" if self.symm is not None else "gather"
 
     def run(self, act, kernel: str = "auto"):
-        from .kernels import spmm as K
-        mr = self.bounds[self.rank][1] - self.bounds[self.rank][0]
-        if mr > 0:
-            K.spmm_exec(self.plan, act, out=self.local[:, :mr], kernel=kernel)
+        m0, m1 = self.bounds[self.rank]
+        if m1 > m0:
+            # the kernel writes its rows straight into the final buffer's columns (ldo = M)
+            self.compute(self.plan, act, self.out[:, m0:m1], kernel)
+        if self.world == 1:
+            return self.out
+        if self.exchange == "symm":
+            # push this block into the same columns of every peer's buffer
+            for p in range(self.world):
+                if p != self.rank and m1 > m0:
+                    peer = self.symm.get_buffer(p, (self.n, self.m), self.dtype)
+                    peer[:, m0:m1].copy_(self.out[:, m0:m1])
+            self.symm.barrier()
+            return self.out
+        if m1 > m0:
+            self.local[:, : m1 - m0].copy_(self.out[:, m0:m1])
         gather_rows(self.gathered, self.local, self.group)
-        return assemble_rows(self.gathered, self.n, self.m, self.world, self.rows_pad, self.bounds)
+        return assemble_rows(self.gathered, self.n, self.m, self.world, self.rows_pad, self.bounds,
+                             out=self.out, skip=self.rank)
 
 
 def gather_rows(gathered, local, group=None):
-    """all_gather of equal-size row shards into [world, N, rows_pad]
+    """all_gather of equal-size row blocks into [world, N, rows_pad]
     (one NCCL all-gather; gloo takes the list form)."""
     import torch.distributed as dist
     if dist.get_backend(group) == "nccl":

@@ -1,7 +1,11 @@
-"""Multi-process (world_size 2, gloo on CPU) tests of the sharding bookkeeping.
+"""Multi-process (world_size 2 and 3, gloo on CPU) tests of the sharding
+bookkeeping.
 
-The per-rank compute is the C oracle here (no GPU in this container); on a
-GPU box the same bookkeeping wraps the product kernel (RowShardedSpmm)."""
+Rows mode runs the product's RowShardedSpmm itself -- plan per shard, the
+rank's block written into the final [N, M] buffer's columns, the all-gather
+exchange and the column placement of the peer blocks -- with the C oracle
+injected as the per-rank compute (no GPU in this container); on a GPU box the
+same object runs the product kernel (tests/test_gpu_parallel.py)."""
 
 import os
 import socket
@@ -37,16 +41,13 @@ def _worker(rank, world, port, mode, q):
         prog = workloads.program("requant_u8", scales, a_zp=2)
         full = oracle.spmm_exec(sw, x, prog, bias)
         if mode == "rows":
-            sh = parallel.shard_rows(sw, world, rank)
-            sp = parallel.shard_program(prog, sh.m0, sh.m1)
-            local = np.zeros((n, sh.rows_pad), np.uint8)
-            if sh.m1 > sh.m0:
-                local[:, : sh.m1 - sh.m0] = oracle.spmm_exec(sh.weight, x, sp, bias[sh.m0: sh.m1])
-            gathered = torch.empty((world, n, sh.rows_pad), dtype=torch.uint8)
-            parallel.gather_rows(gathered, torch.from_numpy(local))
-            bounds = [(parallel.shard_rows(sw, world, r).m0, parallel.shard_rows(sw, world, r).m1)
-                      for r in range(world)]
-            got = parallel.assemble_rows(gathered, n, m, world, sh.rows_pad, bounds).numpy()
+            def oracle_compute(plan, act_kn, out_view, kernel):
+                out_view[...] = torch.from_numpy(oracle.spmm_exec(plan.weight, act_kn, plan.program, plan.bias))
+            rs = parallel.RowShardedSpmm(sw, n, prog, bias=bias, device="cpu", compute=oracle_compute)
+            assert rs.exchange == "gather"
+            got = rs.run(x).numpy()
+            got2 = rs.run(x).numpy()   # reusable across calls
+            assert np.array_equal(got, got2)
         else:
             n0, n1 = parallel.token_shard(n, world, rank)
             part = oracle.spmm_exec(sw, np.ascontiguousarray(x[:, n0:n1]), prog, bias)
@@ -59,9 +60,8 @@ def _worker(rank, world, port, mode, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["rows", "tokens"])
-def test_sharded_equals_single(mode):
-    world = 2
+@pytest.mark.parametrize("mode,world", [("rows", 2), ("rows", 3), ("tokens", 2)])
+def test_sharded_equals_single(mode, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -71,7 +71,7 @@ def test_sharded_equals_single(mode):
     res = dict(q.get(timeout=240) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
-    assert res == {0: True, 1: True}
+    assert res == {r: True for r in range(world)}
 
 
 def test_split_range_covers():

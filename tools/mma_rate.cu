@@ -94,7 +94,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         const uint64_t ed = tc::smem_desc(tc::smem_u32(sm + SM_E), 2048, 128, 0);
         for (int ks = 0; ks < 4; ++ks) {
             bd[ks] = tc::smem_desc_sw128(tc::smem_u32(sm + SM_B) + (sparse ? 64 * (ks & 1) : 32 * ks), 16, 1024);
-            ad[ks] = tc::smem_desc_sw128(tc::smem_u32(sm + SM_A) + 32 * ks, 16, 1024);
+            if (mode & 512)        // K3's 2:4 image: SWIZZLE_NONE core matrices, LBO 128, SBO 512
+                ad[ks] = tc::smem_desc(tc::smem_u32(sm + SM_A) + 256 * (ks & 1), 128, 512, 0);
+            else if (mode & 1024)  // SWIZZLE_64B K-major rows of 64 B
+                ad[ks] = tc::smem_desc(tc::smem_u32(sm + SM_A) + 32 * (ks & 1), 16, 512, 4);
+            else
+                ad[ks] = tc::smem_desc_sw128(tc::smem_u32(sm + SM_A) + 32 * ks, 16, 1024);
         }
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
         t0 = clock64();

@@ -53,11 +53,9 @@ def main():
                                                ctypes.POINTER(ctypes.c_float), ctypes.c_int, ctypes.c_int]
     buf = torch.randint(0, 255, (32 << 20,), dtype=torch.uint8, device="cuda")
     import sys
-    for N, extra, tag in ((224, 16, "sparse SS unrolled"), (224, 16 | 64, "+cp256 per 4 MMA"),
-                          (224, 16 | 128, "+commit per 2 MMA"), (224, 16 | 64 | 128, "+cp256/4 +commit/2"),
-                          (224, 16 | 32 | 128, "+cp128/1 +commit/2 (K3 stage)"),
-                          (128, 16, "N128"), (128, 16 | 256, "N128 alternating accumulators"),
-                          (112, 16 | 256, "N112 alternating accumulators"), (256, 16, "N256")):
+    for N, extra, tag in ((224, 16, "A SW128"), (224, 16 | 512, "A SWIZZLE_NONE (K3 image)"),
+                          (224, 16 | 1024, "A SW64"), (224, 16 | 64 | 128 | 512, "K3 stage, A none"),
+                          (224, 16 | 64 | 128 | 1024, "K3 stage, A SW64"), (224, 16 | 64 | 128, "K3 stage, A SW128")):
         mode = 2 | extra
         run(L, buf, mode, N, 0, iters=1024)
         r = run(L, buf, mode, N, 0)
