@@ -118,6 +118,12 @@ typedef struct {
 } si_plan_info;
 int32_t si_plan_info_get(const void *host_image, si_plan_info *info);
 
+/* Structural validation of `bytes` bytes claiming to be a plan image (e.g.
+ * read from a plan file): header size, magic/version, header consistency and
+ * every section's extent inside the image.  SI_EFORMAT names the defect.
+ * Images from si_plan_image_build always pass. */
+int32_t si_plan_image_validate(const void *image, uint64_t bytes);
+
 /* Device workspace the run needs (0 when none).  For SI_KERNEL_AUTO this is
  * enough for either kernel AUTO may pick (the pick also depends on the
  * alignment of x and ldx, which this query does not see). */

@@ -66,6 +66,7 @@ def lib():
                                      ctypes.POINTER(_u64)]
     L.si_plan_image_build.argtypes = [ctypes.POINTER(SiWeight), ctypes.POINTER(SiProgram), _vp, _vp, _u64]
     L.si_plan_info_get.argtypes = [_vp, ctypes.POINTER(SiPlanInfo)]
+    L.si_plan_image_validate.argtypes = [_vp, _u64]
     L.si_spmm_workspace_size.argtypes = [_vp, _i64, _i32, _i32, ctypes.POINTER(_u64)]
     L.si_spmm_launch_count.argtypes = [_vp, _i64, _i32, _i32]
     L.si_spmm.argtypes = [_vp, _vp, _vp, _i32, _i64, _i64, _vp, _vp, _i64, _vp, _u64, _i32, _vp]
@@ -78,7 +79,7 @@ def lib():
     L.si_bmm_f32.argtypes = [_vp, _vp, _vp] + [_i64] * 14 + [_i32, ctypes.c_float, _vp]
     L.si_quantize_f32.argtypes = [_vp, _i64, ctypes.c_float, _i32, _i32, _i32, _vp, _vp]
     L.si_attention_f32.argtypes = [_vp, _vp] + [_i64] * 6 + [ctypes.c_float, _vp]
-    for f in ("si_plan_image_size", "si_plan_image_build", "si_plan_info_get",
+    for f in ("si_plan_image_size", "si_plan_image_build", "si_plan_info_get", "si_plan_image_validate",
               "si_spmm_workspace_size", "si_spmm_launch_count", "si_spmm",
               "si_spmm_host_workspace_size", "si_spmm_host",
               "si_spmm_host_batch_workspace_size", "si_spmm_host_batch",

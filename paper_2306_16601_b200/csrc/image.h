@@ -15,7 +15,7 @@
 #endif
 
 #define SI_IMG_MAGIC 0x58344953u /* "SI4X" */
-#define SI_IMG_VERSION 4u
+#define SI_IMG_VERSION 5u   /* 5: K2x lists and the K2a row-major W retired (empty sections) */
 #define TR_SLOTS 128 /* K2t residual slots per 256-row pair tile */
 
 // compiled epilogue forms (see plan.cpp: compile_program)

@@ -284,14 +284,7 @@ struct Layout {
     uint64_t total;
 };
 
-// K2 expansion lists (see image.h).  Blocks are bucketed by (row tile, k
-// chunk, k half); duplicate (group, column) pairs are summed per row with
-// int8 wrap-around, as decode_sparse's np.add.at does (sparse.py:130-131).
-struct ExpandLists {
-    std::vector<uint32_t> ptr;   // byte offsets, size nlists + 1
-    std::vector<uint8_t> bytes;
-    int32_t emax = 0;
-};
+
 
 // True when the device's proven-row requant, n(a) = bits(fma(f32(a), c,
 // 1.5*2^23 + zp)) - bits(1.5*2^23) = rint(a*c + zp) (one rounding, exact while
@@ -548,68 +541,6 @@ SparseImages build_sparse_images(const si_weight *w)
     return S;
 }
 
-ExpandLists build_expand_lists(const si_weight *w)
-{
-    ExpandLists e;
-    const int32_t G = w->rows / 4;
-    const int32_t rt_n = (w->logical_rows + 127) / 128;
-    const int32_t kch = (w->cols + 127) / 128;
-    const int64_t nlists = (int64_t)rt_n * kch * 2;
-    std::vector<std::vector<std::pair<uint16_t, uint32_t>>> lists((size_t)nlists);
-    for (int32_t g = 0; g < G; ++g) {
-        const int32_t rt = g / 32, gl = g % 32;
-        if (rt >= rt_n) break;
-        // accumulate this group's blocks by column (handles duplicates)
-        std::vector<std::pair<int32_t, uint32_t>> cols;
-        for (int64_t q = w->group_ptr[g]; q < w->group_ptr[g + 1]; ++q) {
-            uint8_t b[4];
-            bool any = false;
-            for (int r = 0; r < 4; ++r) {
-                b[r] = (uint8_t)w->vals[(q / 4) * 16 + r * 4 + (q % 4)];
-                if (g * 4 + r >= w->logical_rows) b[r] = 0;
-                any |= b[r] != 0;
-            }
-            if (!any) continue;
-            const uint32_t word = (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) | ((uint32_t)b[3] << 24);
-            bool merged = false;
-            for (auto &c : cols)
-                if (c.first == w->idx[q]) {
-                    uint32_t o = c.second, sum = 0;
-                    for (int r = 0; r < 4; ++r)
-                        sum |= (uint32_t)(uint8_t)((int8_t)(o >> (8 * r)) + (int8_t)(word >> (8 * r))) << (8 * r);
-                    c.second = sum;
-                    merged = true;
-                    break;
-                }
-            if (!merged) cols.emplace_back(w->idx[q], word);
-        }
-        for (auto &c : cols) {
-            const int32_t k = c.first, kc = k / 128, kl = k % 128, half = kl / 64;
-            const int32_t ml = 4 * gl;
-            const uint32_t byte = (uint32_t)kl * 128 + ((((uint32_t)ml >> 4) ^ ((uint32_t)kl & 7)) << 4) + (ml & 15);
-            lists[((size_t)rt * kch + kc) * 2 + half].emplace_back((uint16_t)(byte / 4), c.second);
-        }
-    }
-    e.ptr.assign((size_t)nlists + 1, 0);
-    for (int64_t j = 0; j < nlists; ++j) {
-        auto &L = lists[(size_t)j];
-        std::sort(L.begin(), L.end());
-        const size_t n = L.size(), n8 = (n + 7) / 8 * 8;
-        e.ptr[(size_t)j] = (uint32_t)e.bytes.size();
-        e.emax = std::max<int32_t>(e.emax, (int32_t)n8);
-        for (size_t i = 0; i < n8; ++i) {
-            const uint32_t v = L[std::min(i, n - 1)].second;
-            for (int bb = 0; bb < 4; ++bb) e.bytes.push_back((uint8_t)(v >> (8 * bb)));
-        }
-        for (size_t i = 0; i < n8; ++i) {
-            const uint16_t o = L[std::min(i, n - 1)].first;
-            e.bytes.push_back((uint8_t)o);
-            e.bytes.push_back((uint8_t)(o >> 8));
-        }
-    }
-    e.ptr[(size_t)nlists] = (uint32_t)e.bytes.size();
-    return e;
-}
 
 }  // namespace
 
@@ -665,8 +596,7 @@ static int32_t validate(const si_weight *w, const si_program *p)
     return SI_OK;
 }
 
-static Layout make_layout(const si_weight *w, const si_program *p, const Compiled &c, const ExpandLists &x,
-                          const SparseImages &sp)
+static Layout make_layout(const si_weight *w, const si_program *p, const Compiled &c, const SparseImages &sp)
 {
     Layout l{};
     const int64_t G = w->rows / 4, T = w->group_ptr[G], tiles = T / 4;
@@ -697,8 +627,8 @@ static Layout make_layout(const si_weight *w, const si_program *p, const Compile
     put(15, 4 * M);
     put(16, 4 * c.bp.x.size());
     put(17, 2 * c.bp_bucket.size());
-    put(18, 4 * x.ptr.size());
-    put(19, x.bytes.size());
+    put(18, 0);   // (image v4: K2x expansion lists, retired)
+    put(19, 0);
     put(20, 4 * M);
     put(21, sp.img.size());
     put(22, 4 * sp.rptr.size());
@@ -707,7 +637,7 @@ static Layout make_layout(const si_weight *w, const si_program *p, const Compile
     put(25, sp.tr_img.size());
     put(26, 2 * sp.tr_k.size());
     put(27, 4 * sp.tr_cnt.size());
-    put(28, (uint64_t)kp * ((mt + 1) / 2 * 2) * 128);   // whole 256-row pair tiles
+    put(28, 0);   // (image v4: K2a row-major W, retired)
     l.total = cur;
     return l;
 }
@@ -717,9 +647,8 @@ extern "C" int32_t si_plan_image_size(const si_weight *w, const si_program *p, u
     int32_t rc = validate(w, p);
     if (rc) return rc;
     Compiled c = compile_program(p);
-    ExpandLists x = build_expand_lists(w);
     SparseImages sp = build_sparse_images(w);
-    *bytes = make_layout(w, p, c, x, sp).total;
+    *bytes = make_layout(w, p, c, sp).total;
     return SI_OK;
 }
 
@@ -729,9 +658,8 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
     int32_t rc = validate(w, p);
     if (rc) return rc;
     Compiled c = compile_program(p);
-    ExpandLists x = build_expand_lists(w);
     SparseImages sp = build_sparse_images(w);
-    Layout l = make_layout(w, p, c, x, sp);
+    Layout l = make_layout(w, p, c, sp);
     if (bytes < l.total) { si_set_error("image buffer too small"); return SI_ENOSPACE; }
     uint8_t *base = (uint8_t *)host_image;
     std::memset(base, 0, l.total);
@@ -780,10 +708,8 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
     if (!sp.res.empty()) std::memcpy(base + h->off_sp_res, sp.res.data(), 4 * sp.res.size());
     h->off_tc_eptr = l.off[18];
     h->off_tc_ent = l.off[19];
-    h->tc_emax = x.emax;
-    h->tc_nlists = (int32_t)(x.ptr.size() - 1);
-    std::memcpy(base + h->off_tc_eptr, x.ptr.data(), 4 * x.ptr.size());
-    if (!x.bytes.empty()) std::memcpy(base + h->off_tc_ent, x.bytes.data(), x.bytes.size());
+    h->tc_emax = 0;
+    h->tc_nlists = 0;
 
     // micro-tiles: reference layout kept verbatim (sparse.py:28-31)
     int32_t *tp = (int32_t *)(base + h->off_tile_ptr);
@@ -896,11 +822,59 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
                 int8_t v = w->vals[(q / 4) * 16 + r * 4 + (q % 4)];
                 if (m < M && v) wt[(int64_t)w->idx[q] * ldm + m] += v;
             }
-    // K2a source: the same dense W, row-major [mtiles*128][kpad] (k contiguous)
-    int8_t *wr = (int8_t *)(base + h->off_tc_wrow);
-    const int64_t kpad = h->tc_kpad;
-    for (int64_t k = 0; k < kpad; ++k)
-        for (int64_t m = 0; m < ldm; ++m) wr[m * kpad + k] = wt[k * ldm + m];
+    return SI_OK;
+}
+
+// Structural check of an image of `bytes` bytes from an untrusted source (a
+// plan file): header present, magic / version known, every section inside
+// total_bytes, total_bytes inside the buffer, and the section extents the
+// header's own counts imply (the kernels index sections by those counts).
+extern "C" int32_t si_plan_image_validate(const void *image, uint64_t bytes)
+{
+    const SiImage *h = (const SiImage *)image;
+    if (!h || bytes < sizeof(SiImage)) {
+        si_set_error("plan image shorter than its header");
+        return SI_EFORMAT;
+    }
+    if (h->magic != SI_IMG_MAGIC || h->version != SI_IMG_VERSION) {
+        si_set_error("not a plan image (magic/version mismatch)");
+        return SI_EFORMAT;
+    }
+    if (h->total_bytes > bytes || h->total_bytes < sizeof(SiImage)) {
+        si_set_error("plan image total size exceeds the buffer");
+        return SI_EFORMAT;
+    }
+    if (h->M < 1 || h->K < 1 || h->rows < h->M || h->rows % 4 || h->groups != h->rows / 4 || h->padded_blocks < 0 ||
+        h->padded_blocks % 4 || h->tiles * 4 != h->padded_blocks || h->n_ops < 0 || h->n_luts < 0 || h->n_chans < 0 ||
+        h->n_sides < 0 || h->n_bp < 0 || h->tc_mtiles != (h->M + 127) / 128 || h->tc_kpad != (h->K + 127) / 128 * 128) {
+        si_set_error("plan image header fields are inconsistent");
+        return SI_EFORMAT;
+    }
+    const uint64_t M = (uint64_t)h->M, T = (uint64_t)h->padded_blocks, kch = (uint64_t)h->tc_kpad / 128;
+    const uint64_t rt_pad = ((uint64_t)h->tc_mtiles + 1) / 2 * 2;
+    struct Sec { uint64_t off, len; };
+    const Sec secs[] = {
+        {h->off_tile_ptr, 4 * ((uint64_t)h->groups + 1)}, {h->off_tile_w, 4 * T}, {h->off_tile_idx, 4 * T},
+        {h->off_adj, 4 * M}, {h->off_scale_in, 4 * M}, {h->off_ops, 4 * (uint64_t)h->n_ops},
+        {h->off_fparams, 4 * (uint64_t)h->n_ops}, {h->off_finv, 4 * (uint64_t)h->n_ops},
+        {h->off_iparams, 12 * (uint64_t)h->n_ops}, {h->off_luts, 256 * (uint64_t)h->n_luts},
+        {h->off_chans, 4 * (uint64_t)h->n_chans * M}, {h->off_clut, 4 * 256}, {h->off_bp_x, 4 * (uint64_t)h->n_bp},
+        {h->off_bp_v, 4 * ((uint64_t)h->n_bp + 1)}, {h->off_tc_wt, (uint64_t)h->tc_kpad * h->tc_mtiles * 128},
+        {h->off_rqc, 4 * M}, {h->off_bp_key, 4 * (uint64_t)h->n_bp},
+        {h->off_bp_bucket, 2 * (uint64_t)(h->bp_nbucket > 0 ? h->bp_nbucket : 0)}, {h->off_rqg, 4 * M},
+        {h->off_sp_img, rt_pad * kch * 12288}, {h->off_sp_rptr, 4 * ((uint64_t)h->tc_mtiles * 128 + 1)},
+        {h->off_sp_res, 4 * (uint64_t)(h->sp_nres > 0 ? h->sp_nres : 0)}, {h->off_rqp, 4 * M},
+        {h->off_tr_img, rt_pad * 12288}, {h->off_tr_k, 2 * (rt_pad / 2) * TR_SLOTS}, {h->off_tr_cnt, 4 * (rt_pad / 2)},
+    };
+    for (const Sec &sc : secs)
+        if (sc.off > h->total_bytes || sc.len > h->total_bytes - sc.off || sc.off % 16) {
+            si_set_error("plan image section outside the image");
+            return SI_EFORMAT;
+        }
+    if (h->sp_nres < 0 || h->tr_pairs != (int32_t)(rt_pad / 2)) {
+        si_set_error("plan image header fields are inconsistent");
+        return SI_EFORMAT;
+    }
     return SI_OK;
 }
 

@@ -25,12 +25,12 @@
 //    one tcgen05.cp (both metadata tiles, 128x256b) + two MMAs with
 //    descriptors formed by adding offsets to precomputed bases.
 //
-// Roles (20 warps, 96 registers each): warps 0, 14 and 19 TMA producers
+// Roles (20 warps, 96 registers each): warps 0, 14 and 17 TMA producers
 // (stage i on producer i mod 3), warp 1 TMEM allocator + MMA issuer (leader
 // CTA), warps 2-13 the epilogue (3 token-column groups x 4 TMEM lane
-// quarters; the compiled _run_chain forms of k2_common.cuh), warps 15-18 the
-// residual gather (the first also forwards this CTA's X-chunk arrivals to
-// the leader).  8-bit outputs leave per warp: each warp stages its own 32
+// quarters; the compiled _run_chain forms of k2_common.cuh), warps 15, 16,
+// 18, 19 the residual gather (the first also forwards this CTA's X-chunk
+// arrivals to the leader).  8-bit outputs leave per warp: each warp stages its own 32
 // rows x 32 tokens (1 KB, no cross-warp barrier) and TMA-stores them.  TMEM: two 224-column
 // accumulators (the epilogue of tile i overlaps the MMAs of tile i+1) + two
 // 8-column metadata slots.
@@ -54,6 +54,7 @@ enum XsExp : int32_t {
     XE_NO_MMA = 4,      // MMA warp: commits only
     XE_W_TILE0 = 8,     // every W load reads pair tile 0 (L2 hot-spot test)
     XE_NO_STORE = 16,   // epilogue: no TMA stores
+    XE_EPI_LDONLY = 32, // epilogue: TMEM loads + release only (no math, staging, stores)
 };
 
 constexpr int XS_TNH = 112;                          // tokens per CTA
@@ -66,12 +67,19 @@ constexpr int XS_IMG = 12288;                        // one (128-row tile, 128-k
 constexpr int XS_EPI_WARPS = 12;
 constexpr int XS_EPI_GROUPS = XS_EPI_WARPS / 4;
 constexpr int XS_NCH = XS_TN / 32;                   // 32-token epilogue chunks per accumulator (7)
-constexpr int XS_NPROD = 3;                          // warps 0, 14, 19
+// Warp placement: a warp's scheduler (SMSP) is warp % 4.  The MMA issuer
+// (warp 1, SMSP 1) is the critical role: its tcgen05 issue slows when the
+// warps beside it keep the scheduler busy, so no gather warp shares SMSP 1
+// and the producer there (17) sleeps in try_wait instead of spinning.
+constexpr int XS_NPROD = 3;                          // warps 0, 14, 17
 constexpr int XS_PROD1_WARP = 2 + XS_EPI_WARPS;      // 14
-constexpr int XS_GATHER_WARP = XS_PROD1_WARP + 1;    // 15 .. 18
-constexpr int XS_NGATHER = 4;
-constexpr int XS_PROD2_WARP = XS_GATHER_WARP + XS_NGATHER;   // 19
-constexpr int XS_THREADS = 32 * (XS_PROD2_WARP + 1);         // 20 warps: 96 registers each
+constexpr int XS_PROD2_WARP = 17;
+constexpr int XS_NGATHER = 4;                        // warps 15, 16, 18, 19
+constexpr int XS_THREADS = 32 * 20;                  // 20 warps: 96 registers each
+__device__ __forceinline__ int xs_gather_index(int warp)
+{
+    return warp == 15 ? 0 : warp == 16 ? 1 : warp == 18 ? 2 : warp == 19 ? 3 : -1;
+}
 constexpr int XS_WSTG = 32 * 32;                     // 8-bit staging slot of one warp: 32 tokens x 32 m
 constexpr int XS_MAXPAIRS = 512;                     // residual MMA counts staged in smem (M <= 131072)
 constexpr uint32_t XS_ECOL = 2 * XS_TN;              // metadata slots: TMEM columns 448..463
@@ -155,6 +163,22 @@ __device__ __forceinline__ void xs_epi_tile(uint32_t lane_base, int32_t row0, in
         tc::tc_fence_before();
         __syncwarp();
         if (W.lane == 0) release();
+        return;
+    }
+    if (XS_EXP(XE_EPI_LDONLY)) {
+        uint32_t acc = 0;
+#pragma unroll 1
+        for (int ch = W.g; ch < XS_NCH; ch += XS_EPI_GROUPS) {
+            uint32_t r[32];
+            tc::tmem_ld_32x32b_x32(lane_base + ch * 32, r);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc ^= r[j];
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (W.lane == 0) release();
+        if (acc == 0x9e3779b9u && W.lane == 33) *reinterpret_cast<uint32_t *>(P.out) = acc;
         return;
     }
     constexpr bool STAGED = (OUTK == OUT_U8_W || OUTK == OUT_S8_W);
@@ -287,11 +311,11 @@ k3_kernel(const __grid_constant__ CUtensorMap tmap_s, const __grid_constant__ CU
                         continue;
                     }
                     if (i == 0 && s < X.kchunks) {
-                        tc::mbar_spin(&xempty[s], xphase ^ 1);
+                        tc::mbar_wait(&xempty[s], xphase ^ 1);
                         tcw::mbar_expect_tx(&xfull[s], XS_XCH);
                         tcw::tma_load_2d(xbuf + s * XS_XCH, &tmap_x, &xfull[s], s * 128, tok);
                     }
-                    tc::mbar_spin(&empty[stage], phase ^ 1);
+                    tc::mbar_wait(&empty[stage], phase ^ 1);
                     if (rank == 0) tcw::mbar_expect_tx(&full[stage], 2 * XS_IMG);
                     const int rt = 2 * (XS_EXP(XE_W_TILE0) ? 0 : pt) + (int)rank;
                     if (s < X.kchunks)
@@ -377,12 +401,12 @@ k3_kernel(const __grid_constant__ CUtensorMap tmap_s, const __grid_constant__ CU
                 xphase ^= 1;
             }
         }
-    } else if (warp >= XS_GATHER_WARP && warp < XS_GATHER_WARP + XS_NGATHER) {
+    } else if (xs_gather_index(warp) >= 0) {
         // ---------------- residual gather (both CTAs): slot s of the residual
         // operand = activation column tr_k[s] of this CTA's tokens, copied from
         // the resident SW128 X tile into the same layout; forwards this CTA's
         // X-chunk arrivals to the leader (its MMA cannot wait on a peer barrier)
-        const int gi = warp - XS_GATHER_WARP;
+        const int gi = xs_gather_index(warp);
         int tcnt = 0;
         const uint32_t rfull0 = tc::mapa(tc::smem_u32(rfull), 0);
         const uint32_t xpeer0 = tc::mapa(tc::smem_u32(xpeer), 0);

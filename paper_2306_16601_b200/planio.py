@@ -113,10 +113,20 @@ def load_plan(path: str, device=None) -> SpmmPlan:
         n, bn, threads = int(meta["n"]), int(meta["bn"]), int(meta["threads"])
     except KeyError as ex:
         raise PlanFormatError(f"missing field {ex}") from None
-    image = arrs["image"]
-    info = plan_info(image)   # validates the image header (magic / version) natively
-    if image.size < info["image_bytes"]:
-        raise PlanFormatError("plan image shorter than its header says")
+    image = np.ascontiguousarray(arrs["image"], dtype=np.uint8)
+    if image.ndim != 1:
+        raise PlanFormatError("plan image must be a byte vector")
+    # native structural check before anything reads the header: size, magic,
+    # header consistency, every section inside the image
+    from . import _lib
+    if _lib.lib().si_plan_image_validate(_lib.ptr(image), image.nbytes) != 0:
+        raise PlanFormatError("bad plan image: " + _lib.lib().si_last_error().decode(errors="replace"))
+    info = plan_info(image)
+    if info["m"] != sw.logical_rows or info["k"] != sw.cols or info["groups"] != sw.groups \
+            or info["padded_blocks"] != int(sw.group_ptr[-1]):
+        raise PlanFormatError("plan image does not match the packed weight")
+    if info["out_dtype"] != {"f32": 0, "s8": 1, "u8": 2, "s32": 3}[prog.out_dtype.value]:
+        raise PlanFormatError("plan image does not match the program")
     image_dev = torch.from_numpy(image).to(_device(device))
     return SpmmPlan(weight=sw, n=n, bn=bn, num_bn=-(-n // bn), threads=threads,
                     tasks=partition_tasks(sw.groups, -(-n // bn), threads), comp=sw.row_sums(), bias=arrs["bias"],

@@ -68,6 +68,46 @@ def test_corrupt_image_header_is_rejected(tmp_path):
         load_plan(str(p), device="cpu")
 
 
+def _with_image(plan, image):
+    import dataclasses
+    return dataclasses.replace(plan, image=np.ascontiguousarray(image, dtype=np.uint8))
+
+
+@pytest.mark.parametrize("edit", ["short", "section", "total", "m_field"])
+def test_malformed_image_is_rejected_natively(tmp_path, edit):
+    """si_plan_image_validate: a container whose image blob is
+    short, has a section outside the image, claims more bytes than it has,
+    or disagrees with the packed weight fails with PlanFormatError before
+    any kernel could read out of bounds."""
+    from helpers import SiImageHeader
+    import ctypes
+    plan, *_ = _plan()
+    img = plan.image.copy()
+    hdr = SiImageHeader.from_buffer_copy(img[:ctypes.sizeof(SiImageHeader)].tobytes())
+    if edit == "short":
+        img = img[:300]
+    elif edit == "section":
+        off = SiImageHeader.off_tc_wt.offset
+        img[off:off + 8] = np.frombuffer(np.uint64(hdr.total_bytes - 64).tobytes(), np.uint8)
+    elif edit == "total":
+        off = SiImageHeader.total_bytes.offset
+        img[off:off + 8] = np.frombuffer(np.uint64(hdr.total_bytes + 4096).tobytes(), np.uint8)
+    else:
+        off = SiImageHeader.M.offset
+        img[off:off + 4] = np.frombuffer(np.int32(hdr.M - 4).tobytes(), np.uint8)
+    p = tmp_path / "m.si4p"
+    save_plan(_with_image(plan, img), str(p))
+    with pytest.raises(PlanFormatError):
+        load_plan(str(p), device="cpu")
+
+
+def test_built_images_validate():
+    from paper_2306_16601_b200 import _lib
+    for m, k, ratio in ((300, 200, 0.8), (4096, 1024, 0.9), (1, 1, 0.0), (64, 4096, 1.0)):
+        plan, *_ = _plan(m, k, 16, ratio)
+        assert _lib.lib().si_plan_image_validate(_lib.ptr(plan.image), plan.image.nbytes) == 0
+
+
 @pytest.mark.gpu
 def test_loaded_plan_runs_bit_exact(tmp_path):
     from paper_2306_16601_b200 import kernels as K
