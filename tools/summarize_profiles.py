@@ -43,7 +43,7 @@ def launches(tag):
     for (k, g, b), v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"| `{k}` | {g} | {b} | {len(v)} | {sum(v) / len(v) / 1e3:.1f} | {sum(v) / total:.1%} |")
     lines.append("")
-    ours = sum(len(v) for (k, _, _), v in per.items() if k.startswith(("k1", "k2", "kref")))
+    ours = sum(len(v) for (k, _, _), v in per.items() if k.startswith(("k1", "k2", "k3", "kref")))
     lines.append(f"Total launches: {len(rows)}; {ours} of them are this repo's kernels, the rest are torch "
                  f"utility kernels outside the SpMM (buffer fills of the host pipeline's setup).")
     with open(os.path.join(PROF, f"{tag}_launches.md"), "w") as f:
@@ -66,9 +66,9 @@ def raw_csv(path):
     return dict(zip(rows[0], rows[2]))
 
 
-def top(tag, cell="c5b_4096x1024"):
-    rep = os.path.join(OUT, "prof_top.ncu-rep")
-    csvp = os.path.join(OUT, "prof_top_raw.csv")   # exported on the box (tools/gpu_round.sh)
+def top(tag, cell="c5b_4096x1024", which="top", traffic_file=True):
+    rep = os.path.join(OUT, f"prof_{which}.ncu-rep")
+    csvp = os.path.join(OUT, f"prof_{which}_raw.csv")   # exported on the box (tools/gpu_round.sh)
     if os.path.exists(csvp):
         m = raw_csv(csvp)
     elif os.path.exists(rep):
@@ -84,14 +84,20 @@ def top(tag, cell="c5b_4096x1024"):
             "lts__lts2xbar_cycles_active.avg.pct_of_peak_sustained_elapsed",
             "l1tex__m_xbar2l1tex_read_bytes_mem_global_op_tma_ld.sum.pct_of_peak_sustained_elapsed",
             "sm__ops_path_tensor_op_utcimma_src_int8_sparsity_off.avg.pct_of_peak_sustained_elapsed",
+            "sm__ops_path_tensor_op_utcimma_src_int8_sparsity_on.avg.pct_of_peak_sustained_elapsed",
+            "derived__lts__lts2xbar_bytes.sum.per_second", "derived__lts__lts2xbar_bytes.sum.peak_sustained",
+            "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
+            "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
             "Kernel Name"]
-    lines = [f"# {tag}: ncu --set full of the dominant kernel ({cell}, `tests/prof_one.py c5b auto`)", "",
+    lines = [f"# {tag}: ncu --set full of the dominant kernel ({cell}, `tests/prof_one.py c5b tc 3 nk`)", "",
              "| metric | value |", "|---|---|"]
     for k in keys:
         if k in m:
             lines.append(f"| `{k}` | {m[k]} |")
-    with open(os.path.join(PROF, f"{tag}_top.md"), "w") as f:
+    with open(os.path.join(PROF, f"{tag}_{which}.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
+    if not traffic_file:
+        return
 
     def mb(k):
         try:
@@ -114,4 +120,6 @@ if __name__ == "__main__":
     os.makedirs(PROF, exist_ok=True)
     launches(tag)
     top(tag)
+    if os.path.exists(os.path.join(OUT, "prof_sp_raw.csv")):
+        top(tag, which="sp", traffic_file=False)
     print("ok")
