@@ -151,6 +151,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         }
         __threadfence_block();
     }
+    if ((mode & (2048 | 4096)) && warp >= 4 && warp < 12 && !((mode & 4096) && (warp & 3) == 1)) {
+        // busy neighbours: dependent-chain-free FMA/ALU/SHFL mix, like an epilogue
+        float a0 = threadIdx.x, a1 = a0 + 1.f, a2 = a0 + 2.f, a3 = a0 + 3.f;
+        uint32_t u = threadIdx.x;
+        unsigned long long b0 = clock64();
+        while (clock64() - b0 < (unsigned long long)ld_iters) {
+#pragma unroll 16
+            for (int i = 0; i < 64; ++i) {
+                a0 = __fmaf_rn(a0, 1.0001f, 0.5f); a1 = __fmaf_rn(a1, 0.9999f, 0.25f);
+                a2 = __fadd_rn(a2, a3); a3 = __fmul_rn(a3, 1.00001f);
+                u = __byte_perm(u, (uint32_t)i, 0x3715) + __shfl_xor_sync(0xffffffffu, u, 1);
+            }
+        }
+        if (a0 + a1 + a2 + a3 == 1.2345f && u == 7) out[0] = u;
+    }
     if (warp >= 4 && warp < 4 + ldw) {
         // TMEM reader: this warp's lane quarter, 32 columns per load, cycling
         // over the first 256 columns

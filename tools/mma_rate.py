@@ -53,13 +53,13 @@ def main():
                                                ctypes.POINTER(ctypes.c_float), ctypes.c_int, ctypes.c_int]
     buf = torch.randint(0, 255, (32 << 20,), dtype=torch.uint8, device="cuda")
     import sys
-    for N, extra, tag in ((224, 16, "A SW128"), (224, 16 | 512, "A SWIZZLE_NONE (K3 image)"),
-                          (224, 16 | 1024, "A SW64"), (224, 16 | 64 | 128 | 512, "K3 stage, A none"),
-                          (224, 16 | 64 | 128 | 1024, "K3 stage, A SW64"), (224, 16 | 64 | 128, "K3 stage, A SW128")):
+    for N, extra, tag in ((224, 16 | 64 | 128, "K3 stage pattern, idle neighbours"),
+                          (224, 16 | 64 | 128 | 2048, "K3 stage, busy warps on all 4 SMSPs"),
+                          (224, 16 | 64 | 128 | 4096, "K3 stage, busy warps off the issuer's SMSP")):
         mode = 2 | extra
-        run(L, buf, mode, N, 0, iters=1024)
-        r = run(L, buf, mode, N, 0)
-        print(f"{tag:36s} N{N:3d}: {r['cyc_per_mma']:7.1f} clk/MMA  {r['mac_clk_sm']:7.0f} MAC/clk/SM", flush=True)
+        run(L, buf, mode, N, 0, iters=1024, ld_iters=200000)
+        r = run(L, buf, mode, N, 0, ld_iters=3000000)
+        print(f"{tag:44s} N{N:3d}: {r['cyc_per_mma']:7.1f} clk/MMA  {r['mac_clk_sm']:7.0f} MAC/clk/SM", flush=True)
 
 
 if __name__ == "__main__":
