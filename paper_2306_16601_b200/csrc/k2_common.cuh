@@ -227,13 +227,25 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, i
             }
         }
     } else if constexpr (MODE == EPI_DEQ_TABLE) {
+        // dequantized value f32(f64(a) * f64(s)) = RN(a * s) exactly while
+        // |a| <= 2^24; when every row of the warp provably stays below 2^22
+        // (`fast`, the plan's row bound) the magic-number conversion replaces
+        // I2F and the f64 fallback disappears from the loop
+        float x[32];
+        if (fast) {
+            const int32_t adjM = (int32_t)((uint32_t)adj + (uint32_t)MAGIC_I);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                x[j] = __fmul_rn(__fsub_rn(__int_as_float((int32_t)(r[j] + (uint32_t)adjM)), MAGIC_F), s_in);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) x[j] = dev_deq_acc((int32_t)(r[j] + (uint32_t)adj), s_in);
+        }
         // (uniform branch on the plan's bucket occupancy) fixed-step lookups
 #define SI_BP_CHUNK(S)                                                                                          \
-    for (int j = 0; j < 32; ++j) {                                                                              \
-        const float x = dev_deq_acc((int32_t)(r[j] + (uint32_t)adj), s_in);                                    \
-        v[j] = (int32_t)bp_lookup_fixed<S>(x, W.s_key, W.s_bkt, W.s_val, E.n_bp, E.bp_key_lo, E.bp_shift,        \
-                                           E.bp_nbucket);                                                       \
-    }
+    for (int j = 0; j < 32; ++j)                                                                                \
+        v[j] = (int32_t)bp_lookup_fixed<S>(x[j], W.s_key, W.s_bkt, W.s_val, E.n_bp, E.bp_key_lo, E.bp_shift,     \
+                                           E.bp_nbucket);
         if (E.n_bp > 0 && E.bp_occ < 4) {
 #pragma unroll
             SI_BP_CHUNK(2)
@@ -245,23 +257,22 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, i
             SI_BP_CHUNK(6)
         } else {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const float x = dev_deq_acc((int32_t)(r[j] + (uint32_t)adj), s_in);
-                v[j] = (int32_t)bp_lookup_bucketed(x, W.s_key, W.s_bkt, W.s_val, E.n_bp, E.bp_key_lo, E.bp_shift,
+            for (int j = 0; j < 32; ++j)
+                v[j] = (int32_t)bp_lookup_bucketed(x[j], W.s_key, W.s_bkt, W.s_val, E.n_bp, E.bp_key_lo, E.bp_shift,
                                                    E.bp_nbucket);
-            }
         }
 #undef SI_BP_CHUNK
     } else if (E.mode == EPI_DEQ_SIDE) {
         // [DEQ_ACC, ADD_SIDE(i)] (residual connection): f32(f64(a) * f64(s))
         // + side[i][n][m] in f32, the interpreter's two steps without it
         const float *sd = E.sides + (int64_t)__ldg(E.iparams + 3) * E.N * E.M + m;
+        const int32_t adjM = (int32_t)((uint32_t)adj + (uint32_t)MAGIC_I);
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
             const int64_t n = n0 + j;
-            v[j] = (mok && n < P.N)
-                       ? __float_as_int(__fadd_rn(dev_deq_acc((int32_t)(r[j] + (uint32_t)adj), s_in), __ldg(sd + n * E.M)))
-                       : 0;
+            const float d = fast ? __fmul_rn(__fsub_rn(__int_as_float((int32_t)(r[j] + (uint32_t)adjM)), MAGIC_F), s_in)
+                                 : dev_deq_acc((int32_t)(r[j] + (uint32_t)adj), s_in);
+            v[j] = (mok && n < P.N) ? __float_as_int(__fadd_rn(d, __ldg(sd + n * E.M))) : 0;
         }
     } else {
 #pragma unroll
