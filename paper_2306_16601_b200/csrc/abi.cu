@@ -205,6 +205,39 @@ void release_copy_streams(const CopyStreams &cs)
     g_stream_pool.push_back(cs);
 }
 
+// Token chunks of one job.  The batch's first job ramps up (chunk/8, /4, /2
+// before full chunks) and its last job ramps down the same way, so the
+// copy-out stream starts early and the final copy-out is short: with full
+// chunks only, the first H2D and the last D2H run alone on the link.
+std::vector<std::pair<int64_t, int64_t>> job_chunks(int64_t n, int64_t chunk, bool ramp_up, bool ramp_down)
+{
+    std::vector<int64_t> head, tail;
+    for (int d = 8; d >= 2; d /= 2) {
+        const int64_t c = (chunk / d) / 256 * 256;
+        if (c >= 256) {
+            if (ramp_up) head.push_back(c);
+            if (ramp_down) tail.insert(tail.begin(), c);
+        }
+    }
+    int64_t edges = 0;
+    for (int64_t c : head) edges += c;
+    for (int64_t c : tail) edges += c;
+    std::vector<std::pair<int64_t, int64_t>> out;
+    if (n <= edges + chunk) {   // too short to ramp: plain chunks
+        for (int64_t n0 = 0; n0 < n; n0 += chunk) out.emplace_back(n0, n - n0 < chunk ? n - n0 : chunk);
+        return out;
+    }
+    int64_t n0 = 0;
+    for (int64_t c : head) { out.emplace_back(n0, c); n0 += c; }
+    int64_t tail_sum = 0;
+    for (int64_t c : tail) tail_sum += c;
+    const int64_t body_end = n - tail_sum;   // tokens before the ramp-down
+    for (; n0 < body_end; n0 += chunk) out.emplace_back(n0, body_end - n0 < chunk ? body_end - n0 : chunk);
+    n0 = body_end;
+    for (int64_t c : tail) { out.emplace_back(n0, c); n0 += c; }
+    return out;
+}
+
 int32_t check_job(const si_host_job &j, const SiImage *&h)
 {
     h = check_image(j.host_image);
@@ -329,9 +362,10 @@ extern "C" int32_t si_spmm_host_batch(const si_host_job *jobs, int32_t count, vo
         const uint8_t *xh = (const uint8_t *)J.x_host;
         uint8_t *oh = (uint8_t *)J.out_host;
         const int ns = h->n_sides;
-        for (int64_t n0 = 0; n0 < J.n && rc == SI_OK; n0 += L.chunk, ++seq) {
+        const auto chunks = job_chunks(J.n, L.chunk, jb == 0, jb == count - 1);
+        for (size_t ci = 0; ci < chunks.size() && rc == SI_OK; ++ci, ++seq) {
             const int b = (int)(seq % RING);
-            const int64_t nc = J.n - n0 < L.chunk ? J.n - n0 : L.chunk;
+            const int64_t n0 = chunks[ci].first, nc = chunks[ci].second;
             // copy in: buffer b is free once the kernel RING chunks back finished
             if (seq >= RING) cudaStreamWaitEvent(s_in, cmp_done[b], 0);
             cudaError_t e;
