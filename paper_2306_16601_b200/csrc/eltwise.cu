@@ -40,6 +40,7 @@ __device__ __forceinline__ void stage(const float *x, int64_t ld, int64_t rows, 
 // s = sequential f64 sum, out = e * f32(1/s)
 __global__ void k_softmax_rows(const float *x, float *out, int64_t rows, int64_t n, int64_t ld)
 {
+    SI_PDL_ENTRY();
     __shared__ float tile[4][ROWS][CH + 1];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t r0 = ((int64_t)blockIdx.x * 4 + w) * ROWS;
@@ -90,6 +91,7 @@ __global__ void k_softmax_rows(const float *x, float *out, int64_t rows, int64_t
 __global__ void k_layer_norm_rows(const float *x, const float *gamma, const float *beta, double eps, float *out,
                                   int64_t rows, int64_t n)
 {
+    SI_PDL_ENTRY();
     __shared__ float tile[4][ROWS][CH + 1];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t r0 = ((int64_t)blockIdx.x * 4 + w) * ROWS;
@@ -188,6 +190,7 @@ __device__ __forceinline__ void store_rows(float *out, int64_t ld, int64_t rows,
 
 __global__ void k_softmax_rows_smem(const float *x, float *out, int64_t rows, int n)
 {
+    SI_PDL_ENTRY();
     extern __shared__ float t_sm[];
     const int lane = threadIdx.x & 31;
     const int64_t r0 = (int64_t)blockIdx.x * ROWS;
@@ -210,6 +213,7 @@ __global__ void k_softmax_rows_smem(const float *x, float *out, int64_t rows, in
 __global__ void k_layer_norm_rows_smem(const float *x, const float *gamma, const float *beta, double eps, float *out,
                                        int64_t rows, int n)
 {
+    SI_PDL_ENTRY();
     extern __shared__ float t_sm[];
     const int lane = threadIdx.x & 31;
     const int64_t r0 = (int64_t)blockIdx.x * ROWS;
@@ -240,6 +244,7 @@ __global__ void k_layer_norm_rows_smem(const float *x, const float *gamma, const
 __global__ void k_layer_norm_rows_bulk(const float *x, const float *gamma, const float *beta, double eps, float *out,
                                        int64_t rows, int n)
 {
+    SI_PDL_ENTRY();
     extern __shared__ __align__(16) float b_sm[];
     __shared__ __align__(8) uint64_t bar;
     const int lane = threadIdx.x & 31;
@@ -311,6 +316,7 @@ __global__ void __launch_bounds__(256) k_bmm(const float *a, const float *b, flo
                                              int64_t sb1, int64_t ldb, int64_t so0, int64_t so1, int64_t ldo,
                                              int transpose_b, float alpha)
 {
+    SI_PDL_ENTRY();
     __shared__ float As[BK][BT + 4];   // [p][i]
     __shared__ float Bs[BK][BT + 4];   // [p][j]
     const int64_t bz = blockIdx.z, b0 = bz / nb1, b1 = bz % nb1;
@@ -378,6 +384,7 @@ __device__ __forceinline__ uint32_t quant1(float x, double scale, int32_t zp, in
 __global__ void k_quantize4(const float4 *x, int64_t n4, double scale, int32_t zp, int32_t lo, int32_t hi,
                             uint32_t *out)
 {
+    SI_PDL_ENTRY();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
         const float4 v = __ldg(x + i);
         out[i] = quant1(v.x, scale, zp, lo, hi) | quant1(v.y, scale, zp, lo, hi) << 8 |
@@ -388,6 +395,7 @@ __global__ void k_quantize4(const float4 *x, int64_t n4, double scale, int32_t z
 __global__ void k_quantize(const float *x, int64_t n, double scale, int32_t zp, int32_t lo, int32_t hi, void *out,
                            int out_s8)
 {
+    SI_PDL_ENTRY();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         double q = rint(__ddiv_rn((double)x[i], scale)) + (double)zp;
         q = fmin(fmax(q, (double)lo), (double)hi);
@@ -410,10 +418,10 @@ extern "C" int32_t si_softmax_rows_f32(const float *x, float *out, int64_t rows,
     if (rows_fit(n)) {
         const int smem = ROWS * (int)(n + 1) * 4;
         if (smem > 48 * 1024) cudaFuncSetAttribute(k_softmax_rows_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        k_softmax_rows_smem<<<(unsigned)((rows + ROWS - 1) / ROWS), 32, smem, (cudaStream_t)stream>>>(x, out, rows,
+        launch_pdl(k_softmax_rows_smem, dim3((unsigned)((rows + ROWS - 1) / ROWS)), dim3(32), smem, (cudaStream_t)stream, x, out, rows,
                                                                                                        (int)n);
     } else {
-        k_softmax_rows<<<grid_rows(rows), 128, 0, (cudaStream_t)stream>>>(x, out, rows, n, n);
+        launch_pdl(k_softmax_rows, dim3(grid_rows(rows)), dim3(128), 0, (cudaStream_t)stream, x, out, rows, n, n);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { si_set_error(cudaGetErrorString(e)); return SI_ECUDA; }
@@ -434,16 +442,16 @@ extern "C" int32_t si_layer_norm_f32(const float *x, const float *gamma, const f
         const int smem = ROWS * (int)(n + 4) * 4;
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(k_layer_norm_rows_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        k_layer_norm_rows_bulk<<<(unsigned)((rows + ROWS - 1) / ROWS), 32, smem, (cudaStream_t)stream>>>(
+        launch_pdl(k_layer_norm_rows_bulk, dim3((unsigned)((rows + ROWS - 1) / ROWS)), dim3(32), smem, (cudaStream_t)stream, 
             x, gamma, beta, eps, out, rows, (int)n);
     } else if (rows_fit(n)) {
         const int smem = ROWS * (int)(n + 1) * 4;
         if (smem > 48 * 1024)
             cudaFuncSetAttribute(k_layer_norm_rows_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        k_layer_norm_rows_smem<<<(unsigned)((rows + ROWS - 1) / ROWS), 32, smem, (cudaStream_t)stream>>>(
+        launch_pdl(k_layer_norm_rows_smem, dim3((unsigned)((rows + ROWS - 1) / ROWS)), dim3(32), smem, (cudaStream_t)stream, 
             x, gamma, beta, eps, out, rows, (int)n);
     } else {
-        k_layer_norm_rows<<<grid_rows(rows), 128, 0, (cudaStream_t)stream>>>(x, gamma, beta, eps, out, rows, n);
+        launch_pdl(k_layer_norm_rows, dim3(grid_rows(rows)), dim3(128), 0, (cudaStream_t)stream, x, gamma, beta, eps, out, rows, n);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { si_set_error(cudaGetErrorString(e)); return SI_ECUDA; }
@@ -461,7 +469,7 @@ extern "C" int32_t si_bmm_f32(const float *a, const float *b, float *out, int64_
     }
     if (nb0 == 0 || m == 0 || n == 0) return SI_OK;
     dim3 grid((unsigned)((n + BT - 1) / BT), (unsigned)((m + BT - 1) / BT), (unsigned)(nb0 * nb1));
-    k_bmm<<<grid, 256, 0, (cudaStream_t)stream>>>(a, b, out, nb1, m, k, n, sa0, sa1, lda, sb0, sb1, ldb, so0, so1, ldo,
+    launch_pdl(k_bmm, dim3(grid), dim3(256), 0, (cudaStream_t)stream, a, b, out, nb1, m, k, n, sa0, sa1, lda, sb0, sb1, ldb, so0, so1, ldo,
                                                   transpose_b, alpha);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { si_set_error(cudaGetErrorString(e)); return SI_ECUDA; }
@@ -480,11 +488,11 @@ extern "C" int32_t si_quantize_f32(const float *x, int64_t n, float scale, int32
     const int64_t blocks = imin64((n + threads - 1) / threads, 148 * 16);
     if (n % 4 == 0 && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
         const int64_t b4 = imin64((n / 4 + threads - 1) / threads, 148 * 16);
-        k_quantize4<<<(unsigned)b4, threads, 0, (cudaStream_t)stream>>>(reinterpret_cast<const float4 *>(x), n / 4,
+        launch_pdl(k_quantize4, dim3((unsigned)b4), dim3(threads), 0, (cudaStream_t)stream, reinterpret_cast<const float4 *>(x), n / 4,
                                                                        (double)scale, zp, lo, hi,
                                                                        static_cast<uint32_t *>(out));
     } else {
-        k_quantize<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(x, n, (double)scale, zp, lo, hi, out,
+        launch_pdl(k_quantize, dim3((unsigned)blocks), dim3(threads), 0, (cudaStream_t)stream, x, n, (double)scale, zp, lo, hi, out,
                                                                            lo < 0);
     }
     cudaError_t e = cudaGetLastError();
@@ -511,6 +519,7 @@ constexpr int AT_SMEM = (AT_QK + AT_S * AT_D) * 4;
 __global__ void __launch_bounds__(256, 2) k_attention(const float *qkv, float *ctx, int64_t seq, int64_t heads,
                                                       int64_t d, int64_t ld, int64_t ldo, float alpha)
 {
+    SI_PDL_ENTRY();
     extern __shared__ __align__(16) float sm[];
     float *Qs = sm;                    // [S][D+4]
     float *Ks = sm + AT_S * AT_LQ;     // [S][D+4]
@@ -687,7 +696,7 @@ extern "C" int32_t si_attention_f32(const float *qkv, float *ctx, int64_t batch,
     const int smem = AT_SMEM;
     // (cheap; set on every call so every device of the process has it)
     cudaFuncSetAttribute(k_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_attention<<<(unsigned)(batch * heads), 256, smem, (cudaStream_t)stream>>>(qkv, ctx, seq, heads, head_dim, ld_qkv,
+    launch_pdl(k_attention, dim3((unsigned)(batch * heads)), dim3(256), smem, (cudaStream_t)stream, qkv, ctx, seq, heads, head_dim, ld_qkv,
                                                                                ld_ctx, alpha);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { si_set_error(cudaGetErrorString(e)); return SI_ECUDA; }

@@ -8,6 +8,37 @@
 
 void si_set_error(const std::string &msg);
 
+#ifdef __CUDACC__
+#include <cuda_runtime.h>
+#include <utility>
+// Launch with programmatic stream serialization (PDL): the kernel's prologue
+// (barrier init, TMEM allocation, descriptor prefetch) overlaps the tail of
+// the previous kernel on the stream; every kernel launched this way calls
+// tc::pdl_wait() before its first access to data another kernel produced.
+// kernel entry of a PDL-launched kernel with no prologue worth overlapping
+#define SI_PDL_ENTRY()                                                      \
+    do {                                                                    \
+        asm volatile("griddepcontrol.wait;" ::: "memory");                 \
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");    \
+    } while (0)
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+#endif
+
 struct SpmmArgs {
     const SiImage *h;       // host copy of the header
     const void *img;        // device image

@@ -52,6 +52,7 @@ k1_gather_kernel(const int32_t *__restrict__ tile_ptr, const uint4 *__restrict__
                  const int4 *__restrict__ tile_idx, int32_t groups, const uint8_t *__restrict__ x,
                  int64_t ldx, int64_t N, void *__restrict__ out, int64_t ldo, EpiParams E)
 {
+    SI_PDL_ENTRY();
     __shared__ uint32_t stage[K1_ROWS][K1_TOK + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int32_t g = blockIdx.y * K1_WARPS + warp;
@@ -122,6 +123,7 @@ k1_gather_kernel(const int32_t *__restrict__ tile_ptr, const uint4 *__restrict__
 __global__ void transpose_nk_kernel(const uint8_t *__restrict__ x, int64_t ldx, int64_t N, int32_t K,
                                     uint8_t *__restrict__ xt, int64_t ldt)
 {
+    SI_PDL_ENTRY();
     __shared__ uint8_t tile[64][65];
     const int64_t n0 = (int64_t)blockIdx.x * 64;
     const int32_t k0 = blockIdx.y * 64;
@@ -148,6 +150,7 @@ __global__ void ref_kernel(const int32_t *__restrict__ tile_ptr, const int8_t *_
                            const int32_t *__restrict__ idx, const uint8_t *__restrict__ x, int32_t layout,
                            int64_t ldx, int64_t N, void *__restrict__ out, int64_t ldo, EpiParams E)
 {
+    SI_PDL_ENTRY();
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= N * (int64_t)E.M) return;
     const int64_t n = e / E.M;
@@ -178,10 +181,10 @@ void launch_k1_mode(const SpmmArgs &a, const uint8_t *x, int64_t ldx, bool vec, 
     auto tw = img_sec<uint4>(a.img, h->off_tile_w);
     auto ti = img_sec<int4>(a.img, h->off_tile_idx);
     if (vec)
-        k1_gather_kernel<MODE, OUTB, true><<<grid, K1_WARPS * 32, 0, st>>>(tp, tw, ti, h->groups, x, ldx, a.n,
+        launch_pdl(k1_gather_kernel<MODE, OUTB, true>, dim3(grid), dim3(K1_WARPS * 32), 0, st, tp, tw, ti, h->groups, x, ldx, a.n,
                                                                           a.out, a.ldo, E);
     else
-        k1_gather_kernel<MODE, OUTB, false><<<grid, K1_WARPS * 32, 0, st>>>(tp, tw, ti, h->groups, x, ldx, a.n,
+        launch_pdl(k1_gather_kernel<MODE, OUTB, false>, dim3(grid), dim3(K1_WARPS * 32), 0, st, tp, tw, ti, h->groups, x, ldx, a.n,
                                                                            a.out, a.ldo, E);
 }
 
@@ -217,7 +220,7 @@ int k1_launch(const SpmmArgs &a)
     if (a.layout == 1) {
         const int64_t ldt = tpad(a.n);
         dim3 grid((unsigned)((ldt + 63) / 64), (unsigned)((a.h->K + 63) / 64));
-        transpose_nk_kernel<<<grid, dim3(32, 8), 0, st>>>(a.x, a.ldx, a.n, a.h->K, (uint8_t *)a.ws, ldt);
+        launch_pdl(transpose_nk_kernel, dim3(grid), dim3(dim3(32, 8)), 0, st, a.x, a.ldx, a.n, a.h->K, (uint8_t *)a.ws, ldt);
         x = (const uint8_t *)a.ws;
         ldx = ldt;
     }
@@ -237,7 +240,7 @@ int kref_launch(const SpmmArgs &a)
     EpiParams E = make_epi(h, a.img, a.sides, a.n);
     const int64_t total = a.n * (int64_t)h->M;
     const unsigned blocks = (unsigned)((total + 255) / 256);
-    ref_kernel<<<blocks, 256, 0, st>>>(img_sec<int32_t>(a.img, h->off_tile_ptr),
+    launch_pdl(ref_kernel, dim3(blocks), dim3(256), 0, st, img_sec<int32_t>(a.img, h->off_tile_ptr),
                                        img_sec<int8_t>(a.img, h->off_tile_w),
                                        img_sec<int32_t>(a.img, h->off_tile_idx), a.x, a.layout, a.ldx, a.n,
                                        a.out, a.ldo, E);

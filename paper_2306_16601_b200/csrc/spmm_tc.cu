@@ -88,6 +88,8 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    tc::pdl_wait();                 // X may come from the previous kernel
+    tc::pdl_launch_dependents();
 
     const int prod = producer_index(warp, 2 + EPI_WARPS);
     // (a producer must never run more than one ring round ahead of the
@@ -233,6 +235,8 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
     tc::cluster_sync();
     tc::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    tc::pdl_wait();                 // X may come from the previous kernel
+    tc::pdl_launch_dependents();
 
     const int prod = producer_index(warp, 2 + EPI_WARPS);
     // (a producer must never run more than one ring round ahead of the
@@ -346,7 +350,7 @@ int launch_mode(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx,
         static_assert(smem <= SMEM_MAX, "shared memory budget");
         set_smem_attr(kern, smem);
         const int tiles = p.mtiles * p.ntiles;
-        kern<<<tiles < sms ? tiles : sms, MT_THREADS, smem, st>>>(tw, tx, to, p, E);
+        return (int)launch_pdl(kern, dim3(tiles < sms ? tiles : sms), dim3(MT_THREADS), smem, st, tw, tx, to, p, E);
     } else {
         auto kern = k2p_kernel<MODE, OUTK>;
         constexpr int smem = pair_smem<MODE, OUTK>();
@@ -354,7 +358,7 @@ int launch_mode(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx,
         set_smem_attr(kern, smem);
         const int units = p.mtiles * p.ntiles;
         const int pairs = units < sms / 2 ? units : sms / 2;
-        kern<<<2 * pairs, MT_THREADS, smem, st>>>(tw, tx, to, p, E);
+        return (int)launch_pdl(kern, dim3(2 * pairs), dim3(MT_THREADS), smem, st, tw, tx, to, p, E);
     }
     return (int)cudaGetLastError();
 }

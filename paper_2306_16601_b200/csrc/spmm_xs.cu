@@ -246,6 +246,8 @@ k3_kernel(const __grid_constant__ CUtensorMap tmap_s, const __grid_constant__ CU
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(rempty + 1);
     // per pair tile residual MMA counts, read by every role once per row tile
     int32_t *s_rcnt = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(full) + 1024);
+    tc::pdl_wait();                 // X may come from the previous kernel (PDL launch)
+    tc::pdl_launch_dependents();
     for (int i = threadIdx.x; i < X.ptiles; i += blockDim.x) s_rcnt[i] = __ldg(X.tr_cnt + i);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -512,8 +514,7 @@ int k3_launch_mode(const SpmmArgs &a, const CUtensorMap &ts, const CUtensorMap &
     X.mgroups = pick_mgroups(X.ptiles, X.ntiles, npairs);
     const long units = (long)X.ntiles * X.mgroups;
     const int pairs = units < npairs ? (int)units : npairs;
-    kern<<<2 * pairs, XS_THREADS, smem, st>>>(ts, tr, tx, to, p, E, X);
-    return (int)cudaGetLastError();
+    return (int)launch_pdl(kern, dim3(2 * pairs), dim3(XS_THREADS), smem, st, ts, tr, tx, to, p, E, X);
 }
 
 template <int OUTK>

@@ -359,6 +359,17 @@ __device__ __forceinline__ void mbar_spin_cluster(uint64_t *b, uint32_t parity)
 }  // namespace tc
 
 namespace tc {
+// Programmatic dependent launch: a kernel launched with programmatic stream
+// serialization may start while the previous kernel on the stream drains;
+// pdl_wait() blocks until that kernel has completed and its writes are
+// visible (call it before touching memory it may have produced),
+// pdl_launch_dependents() lets the next kernel's CTAs start on SMs this grid
+// frees (they block in their own pdl_wait until this grid completes).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+}  // namespace tc
+
+namespace tc {
 // 1-D bulk copy global -> this CTA's smem, completing bytes on an mbarrier
 __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
 {
