@@ -16,7 +16,7 @@
 
 #define SI_IMG_MAGIC 0x58344953u /* "SI4X" */
 #define SI_IMG_VERSION 5u   /* 5: K2x lists and the K2a row-major W retired (empty sections) */
-#define TR_SLOTS 128 /* K2t residual slots per 256-row pair tile */
+#define TR_SLOTS 128 /* K3 residual slots per 256-row pair tile */
 
 // compiled epilogue forms (see plan.cpp: compile_program)
 enum EpiMode : int32_t {
@@ -79,7 +79,7 @@ struct SiImage {
                              //                         1 requant rounding proven exact (plan.cpp
                              //                         requant_row_exact), else the requant certificate
                              //                         guard 2^-22 max|r| (<= 1/4; 0 for other modes)
-    // K2s (2:4 sparse tensor cores): per (128-row tile, 128-k chunk) a 12 KB
+    // 2:4 images (K3, spmm_xs.cu): per (128-row tile, 128-k chunk) a 12 KB
     // image = compressed A [128 rows x 64 B] (K-major, SWIZZLE_NONE core
     // matrices, LBO 128 / SBO 512) + two metadata tiles [128 rows x 16 B]
     // (bytes 0-7: 4-bit idx0|idx1<<2 per 4-wide k window; SBO 128), and
@@ -90,14 +90,14 @@ struct SiImage {
     int32_t sp_nres, sp_maxres;  // residual entries, max per row
     uint64_t off_rqp;        // f32   [M]               requant multiplier c' of rows proven exact (rqg == 1):
                              //                         out = bits(fma(f32(a), c', 1.5*2^23 + zp)) - bits(1.5*2^23)
-    // K2t (X-stationary 2:4 kernel) residual operand, per 256-row pair tile
+    // K3 (X-stationary 2:4 kernel) residual operand, per 256-row pair tile
     // pt: the columns that did not fit the main 2:4 images, gathered on-chip
     // into TR_SLOTS slots of a second 2:4 operand (plan.cpp build_tr_sections)
     uint64_t off_tr_img;     // bytes [2*pairs][12288]   residual 2:4 images (same format as sp_img)
     uint64_t off_tr_k;       // u16   [pairs][TR_SLOTS]   activation column of each slot
     uint64_t off_tr_cnt;     // i32   [pairs]             residual MMAs (64 slots each; 0..TR_SLOTS/64)
-    int32_t tr_ok, tr_pairs; // tr_ok 0: some pair tile needs more than TR_SLOTS slots (K2t unavailable)
-    uint64_t off_tc_wrow;    // int8  [tc_mtiles*128][tc_kpad] dense W row-major (K2a: rows loaded into TMEM)
+    int32_t tr_ok, tr_pairs; // tr_ok 0: some pair tile needs more than TR_SLOTS slots (K3 unavailable)
+    uint64_t off_tc_wrow;    // (image v4: row-major W of the retired K2a; empty since v5)
 };
 
 static_assert(sizeof(SiImage) % 16 == 0, "image header must stay 16-byte aligned");

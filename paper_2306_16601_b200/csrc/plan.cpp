@@ -342,7 +342,7 @@ static float requant_find_multiplier(int64_t A, float s_in, float fp, int32_t zp
     return 0.0f;
 }
 
-// K2s 2:4 images (see image.h).  A window (group, 4 consecutive k) keeps
+// 2:4 images of K3 (see image.h).  A window (group, 4 consecutive k) keeps
 // its first two nonzero columns in the compressed operand; further columns
 // go to the per-row residual lists.
 struct SparseImages {
@@ -350,7 +350,7 @@ struct SparseImages {
     std::vector<int32_t> rptr;
     std::vector<int32_t> res;
     int32_t maxres = 0;
-    // K2t residual operand (image.h): per 256-row pair tile
+    // K3 residual operand (image.h): per 256-row pair tile
     std::vector<uint8_t> tr_img;    // [pair tiles * 2][12288]
     std::vector<uint16_t> tr_k;     // [pair tiles][TR_SLOTS]
     std::vector<int32_t> tr_cnt;    // [pair tiles] residual MMAs (64 slots each)
@@ -381,12 +381,12 @@ static void sp_put_window(uint8_t *tile, int32_t row, int32_t wl, const std::pai
     *e = (uint8_t)((*e & ((wm % 2) ? 0x0F : 0xF0)) | ((wm % 2) ? (nib << 4) : nib));
 }
 
-// K2t: the residual columns of a 256-row pair tile become one more 2:4
+// K3: the residual columns of a 256-row pair tile become one more 2:4
 // operand over "slots": slot s holds activation column tr_k[s] (gathered
 // on-chip from the resident X tile), so the residual is one or two extra
 // sparse MMAs instead of per-element epilogue work.  Slots are assigned
 // greedily so that no row holds more than two entries in any 4-slot window;
-// a pair tile needing more than TR_SLOTS slots disables K2t (tr_ok = 0).
+// a pair tile needing more than TR_SLOTS slots disables K3 (tr_ok = 0).
 static void build_tr_sections(SparseImages &S, const std::vector<std::vector<int32_t>> &rres, int32_t rt_n,
                               int32_t rt_pad)
 {

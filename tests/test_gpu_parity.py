@@ -376,3 +376,24 @@ def test_host_entry_concurrent_threads():
     assert not errors, errors
     for i in range(2):
         check_equal(results[i], cases[i][2], cases[i][3], ("thread", i))
+
+
+@pytest.mark.parametrize("kernel", ["auto", "gather", "tc", "sp"])
+@pytest.mark.parametrize("col0", [0, 16, 3])
+def test_output_into_wider_buffer(kernel, col0):
+    """out may be a column block of a wider [N, ldo] buffer (ldo > M, base
+    offset col0): the row-shard write path (parallel.RowShardedSpmm).  A
+    16-byte-aligned block takes the TMA-store epilogue, col0 = 3 the direct
+    stores; the columns around the block stay untouched."""
+    m, k, n = 1024, 1024, 1000
+    w, x, bias, scales = baseline_inputs(m, k, n, 0.9, 71)
+    sw = P.encode_sparse(w, scales)
+    prog = workloads.program("requant_u8", scales)
+    plan = K.plan_spmm(sw, n, program=prog, bias=bias)
+    act = K.relayout_tokens(np.ascontiguousarray(x.T))
+    wide = torch.full((n, m + 48), 0x5A, dtype=torch.uint8, device="cuda")
+    view = wide[:, col0: col0 + m]
+    K.spmm_exec(plan, act, out=view, kernel=kernel)
+    got = wide.cpu().numpy()
+    check_equal(got[:, col0: col0 + m], oracle.spmm_exec(sw, x, prog, bias), prog, (kernel, col0))
+    assert (got[:, :col0] == 0x5A).all() and (got[:, col0 + m:] == 0x5A).all()

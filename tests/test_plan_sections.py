@@ -1,6 +1,6 @@
 """CPU checks of plan-image sections that the GPU kernels rely on:
 the requant exactness proof (plan.cpp requant_row_exact) and the 2:4
-images + residual lists of the sparse tensor-core kernel (K2s)."""
+images + residual lists of the 2:4 tensor-core images (K3)."""
 
 import numpy as np
 import pytest
@@ -102,7 +102,7 @@ def _decode_sp_tile(t):
 
 @pytest.mark.parametrize("m,k,ratio", [(1024, 1024, 0.9), (520, 272, 0.8), (768, 768, 0.85), (4096, 1024, 0.9)])
 def test_k2t_residual_operand_reconstructs_weight(m, k, ratio):
-    """K2t: main 2:4 images + the per-pair-tile residual operand over slots
+    """K3: main 2:4 images + the per-pair-tile residual operand over slots
     (slot s = activation column tr_k[s]) sum to W exactly; slots beyond the
     tile's residual MMA count carry no weight."""
     w, _, _, img = _plan(m, k, ratio, 7, "s32")
