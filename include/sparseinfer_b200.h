@@ -58,7 +58,8 @@ typedef enum {
     SI_KERNEL_GATHER = 1,  /* K1: CUDA-core dp4a gather over 4x1 micro-tiles */
     SI_KERNEL_TC = 2,      /* K2: tcgen05 kind::i8 tensor-core tiles, dense-expanded W */
     SI_KERNEL_REF = 3,     /* naive per-element kernel (spmm_ref, spmm.py:401) */
-    SI_KERNEL_SP = 4       /* K3: tcgen05.mma.sp 2:4 W images, X-stationary (token-major X, K <= 1024) */
+    SI_KERNEL_SP = 4,      /* K3: tcgen05.mma.sp 2:4 W images, X-stationary (token-major X, K <= 1024) */
+    SI_KERNEL_WS = 5       /* K4: tcgen05.mma.sp 2:4 W images resident per CTA pair, X streamed (token-major X, K <= 1024) */
 } si_kernel;
 
 /* Host view of a Sparse4x1Weight (sparse.py:23-41). */

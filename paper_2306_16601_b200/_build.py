@@ -26,7 +26,7 @@ EXTRA_DEFS = os.environ.get("SI_BUILD_DEFS", "").split()
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off",
               "-Xptxas", "-v", "--expt-relaxed-constexpr"]
-SOURCES = ["plan.cpp", "abi.cu", "spmm_gather.cu", "spmm_tc.cu", "spmm_xs.cu", "eltwise.cu"]
+SOURCES = ["plan.cpp", "abi.cu", "spmm_gather.cu", "spmm_tc.cu", "spmm_xs.cu", "spmm_ws.cu", "eltwise.cu"]
 
 
 def nvcc() -> str:

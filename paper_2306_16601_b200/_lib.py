@@ -14,7 +14,7 @@ import numpy as np
 from . import _build
 
 SI_OK, SI_EINVAL, SI_EFORMAT, SI_ECUDA, SI_EUNSUPPORTED, SI_ENOSPACE = range(6)
-KERNELS = {"auto": 0, "gather": 1, "tc": 2, "ref": 3, "sp": 4}
+KERNELS = {"auto": 0, "gather": 1, "tc": 2, "ref": 3, "sp": 4, "ws": 5}
 LAYOUTS = {"kn": 0, "nk": 1}
 
 _vp, _i32, _i64, _u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64

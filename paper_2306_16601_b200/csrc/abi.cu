@@ -102,7 +102,7 @@ extern "C" int32_t si_spmm(const void *host_image, const void *dev_image, const 
         si_set_error("program needs side inputs");
         return SI_EINVAL;
     }
-    if (kernel < SI_KERNEL_AUTO || kernel > SI_KERNEL_SP) {
+    if (kernel < SI_KERNEL_AUTO || kernel > SI_KERNEL_WS) {
         si_set_error("unknown kernel id");
         return SI_EINVAL;
     }
@@ -120,11 +120,16 @@ extern "C" int32_t si_spmm(const void *host_image, const void *dev_image, const 
         si_set_error("2:4 kernel needs token-major 16-byte-aligned activations, K <= 1024, >= 2 row tiles");
         return SI_EUNSUPPORTED;
     }
+    if (k == SI_KERNEL_WS && !k4_supported(h, n, x_layout, x, ldx)) {
+        si_set_error("W-stationary 2:4 kernel needs token-major 16-byte-aligned activations, K <= 1024, >= 2 row tiles");
+        return SI_EUNSUPPORTED;
+    }
     SpmmArgs a{h, dev_image, (const uint8_t *)x, x_layout, ldx, n, sides, out, ldo, workspace, workspace_bytes,
                stream};
     int err = k == SI_KERNEL_GATHER ? k1_launch(a)
             : k == SI_KERNEL_TC     ? k2_launch(a)
             : k == SI_KERNEL_SP     ? k3_launch(a)
+            : k == SI_KERNEL_WS     ? k4_launch(a)
                                     : kref_launch(a);
     if (err != cudaSuccess) {
         si_set_error(std::string("CUDA launch failed: ") + cudaGetErrorString((cudaError_t)err));

@@ -15,7 +15,7 @@
 #endif
 
 #define SI_IMG_MAGIC 0x58344953u /* "SI4X" */
-#define SI_IMG_VERSION 5u   /* 5: K2x lists and the K2a row-major W retired (empty sections) */
+#define SI_IMG_VERSION 6u   /* 6: unused residual slots carry tr_k = 0xFFFF */
 #define TR_SLOTS 128 /* K3 residual slots per 256-row pair tile */
 
 // compiled epilogue forms (see plan.cpp: compile_program)
@@ -94,7 +94,7 @@ struct SiImage {
     // pt: the columns that did not fit the main 2:4 images, gathered on-chip
     // into TR_SLOTS slots of a second 2:4 operand (plan.cpp build_tr_sections)
     uint64_t off_tr_img;     // bytes [2*pairs][12288]   residual 2:4 images (same format as sp_img)
-    uint64_t off_tr_k;       // u16   [pairs][TR_SLOTS]   activation column of each slot
+    uint64_t off_tr_k;       // u16   [pairs][TR_SLOTS]   activation column of each slot (0xFFFF: unused)
     uint64_t off_tr_cnt;     // i32   [pairs]             residual MMAs (64 slots each; 0..TR_SLOTS/64)
     int32_t tr_ok, tr_pairs; // tr_ok 0: some pair tile needs more than TR_SLOTS slots (K3 unavailable)
     uint64_t off_tc_wrow;    // (image v4: row-major W of the retired K2a; empty since v5)

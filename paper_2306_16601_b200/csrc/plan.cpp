@@ -424,7 +424,7 @@ static void build_tr_sections(SparseImages &S, const std::vector<std::vector<int
         }
         if (!S.tr_ok) break;
         S.tr_cnt[pt] = (used + 63) / 64;
-        for (int32_t s = 0; s < TR_SLOTS; ++s) S.tr_k[(size_t)pt * TR_SLOTS + s] = (uint16_t)std::max(slot_col[s], 0);
+        for (int32_t s = 0; s < TR_SLOTS; ++s) S.tr_k[(size_t)pt * TR_SLOTS + s] = slot_col[s] >= 0 ? (uint16_t)slot_col[s] : (uint16_t)0xFFFF;
         // per row and window: the (position, value) entries
         std::vector<std::vector<std::pair<int32_t, uint8_t>>> win((size_t)256 * (TR_SLOTS / 4));
         for (int32_t s = 0; s < TR_SLOTS; ++s)

@@ -71,3 +71,7 @@ int k2_launch_count(const SiImage *h, int32_t layout);
 // K3: X-stationary 2:4-sparse tensor-core kernel (spmm_xs.cu): token-major X, K <= 1024
 int k3_launch(const SpmmArgs &a);
 bool k3_supported(const SiImage *h, int64_t n, int32_t layout, const void *x, int64_t ldx);
+
+// K4: W-stationary 2:4-sparse tensor-core kernel (spmm_ws.cu): token-major X, K <= 1024
+int k4_launch(const SpmmArgs &a);
+bool k4_supported(const SiImage *h, int64_t n, int32_t layout, const void *x, int64_t ldx);

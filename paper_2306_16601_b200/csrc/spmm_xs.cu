@@ -431,7 +431,10 @@ k3_kernel(const __grid_constant__ CUtensorMap tmap_s, const __grid_constant__ CU
                 uint32_t kk4[4], kofs[4], kx[4];
                 const uint16_t *kp = X.tr_k + (size_t)pt * TR_SLOTS + 4 * j4;
 #pragma unroll
-                for (int b = 0; b < 4; ++b) kk4[b] = __ldg(kp + b);
+                for (int b = 0; b < 4; ++b) {
+                    kk4[b] = __ldg(kp + b);
+                    if (kk4[b] == 0xFFFFu) kk4[b] = 0;     // unused slot: any column (its weights are zero)
+                }
                 tc::mbar_wait(rempty, rphase ^ 1);
                 if (lane == 0 && rank == 0) XS_TRACE(13 + gi, tcnt, 8);
 #pragma unroll

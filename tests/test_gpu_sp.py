@@ -1,5 +1,6 @@
-"""GPU parity of K3, the X-stationary 2:4-sparse tensor-core kernel
-(csrc/spmm_xs.cu, kernel="sp"), against the C oracle -- bit-exact for every
+"""GPU parity of the 2:4-sparse tensor-core kernels -- K3, X-stationary
+(csrc/spmm_xs.cu, kernel="sp"), and K4, W-stationary (csrc/spmm_ws.cu,
+kernel="ws") -- against the C oracle -- bit-exact for every
 epilogue form it compiles, on shapes ragged against its 256-row pair tiles,
 128-k chunks and 224-token tiles, with residual operands (windows holding
 more than two nonzero columns of a group) of zero, one and two MMAs."""
@@ -28,15 +29,16 @@ def _sp_applies(plan) -> bool:
     return h.tr_ok == 1 and h.tc_kpad <= 1024 and h.tc_mtiles >= 2 and h.K % 16 == 0
 
 
+@pytest.mark.parametrize("kernel", ["sp", "ws"])
 @pytest.mark.parametrize("m,k,n,ratio,kind", CASES)
-def test_sp_kernel_bit_exact(m, k, n, ratio, kind):
+def test_sp_kernel_bit_exact(m, k, n, ratio, kind, kernel):
     w, x, bias, scales = baseline_inputs(m, k, n, ratio, 900 + m + k + n)
     sw = P.encode_sparse(w, scales)
     prog = workloads.program(kind, scales, a_zp=2)
     plan = K.plan_spmm(sw, n, program=prog, bias=bias)
     assert _sp_applies(plan), (m, k, n, ratio)
     act = K.relayout_tokens(np.ascontiguousarray(x.T))
-    got = K.spmm_exec(plan, act, kernel="sp").cpu().numpy()
+    got = K.spmm_exec(plan, act, kernel=kernel).cpu().numpy()
     want = oracle.spmm_exec(sw, x, prog, bias)
     if want.dtype == np.float32 and kind.startswith("gelu") and not kind.endswith("u8"):
         np.testing.assert_allclose(got, want, rtol=1e-5, atol=0)
@@ -58,15 +60,16 @@ def test_sp_residual_counts_covered():
     assert {0, 1, 2} <= seen, seen
 
 
-def test_sp_unsupported_is_refused():
+@pytest.mark.parametrize("kernel", ["sp", "ws"])
+def test_sp_unsupported_is_refused(kernel):
     """[K, N] activations and K > 1024 are not K3's: an explicit request is
     refused (RuntimeError from SI_EUNSUPPORTED), AUTO routes elsewhere."""
     w, x, bias, scales = baseline_inputs(512, 2048, 300, 0.9, 5)
     sw = P.encode_sparse(w, scales)
     plan = K.plan_spmm(sw, 300, bias=bias)
     with pytest.raises(RuntimeError):
-        K.spmm_exec(plan, K.relayout_tokens(np.ascontiguousarray(x.T)), kernel="sp")
+        K.spmm_exec(plan, K.relayout_tokens(np.ascontiguousarray(x.T)), kernel=kernel)
     with pytest.raises(RuntimeError):
-        K.spmm_exec(plan, K.relayout_activation(x), kernel="sp")
+        K.spmm_exec(plan, K.relayout_activation(x), kernel=kernel)
     got = K.spmm_exec(plan, K.relayout_tokens(np.ascontiguousarray(x.T))).cpu().numpy()
     assert np.array_equal(got, oracle.spmm_exec(sw, x, K.raw_program(sw), bias))

@@ -103,8 +103,8 @@ def _decode_sp_tile(t):
 @pytest.mark.parametrize("m,k,ratio", [(1024, 1024, 0.9), (520, 272, 0.8), (768, 768, 0.85), (4096, 1024, 0.9)])
 def test_k2t_residual_operand_reconstructs_weight(m, k, ratio):
     """K3: main 2:4 images + the per-pair-tile residual operand over slots
-    (slot s = activation column tr_k[s]) sum to W exactly; slots beyond the
-    tile's residual MMA count carry no weight."""
+    (slot s = activation column tr_k[s], 0xFFFF when unused) sum to W exactly;
+    slots beyond the tile's residual MMA count carry no weight."""
     w, _, _, img = _plan(m, k, ratio, 7, "s32")
     h = image_header(img)
     assert h.tr_ok == 1
@@ -124,6 +124,10 @@ def test_k2t_residual_operand_reconstructs_weight(m, k, ratio):
         used = 64 * cnt[rt // 2]
         assert not R[:, used:].any()
         for s in range(used):
+            if trk[rt // 2, s] == 0xFFFF:              # unused slot: no weight
+                assert not R[:, s].any()
+                continue
             D[rt * 128:(rt + 1) * 128, trk[rt // 2, s]] += R[:, s]
+        assert (trk[rt // 2, used:] == 0xFFFF).all()
     np.testing.assert_array_equal(D[:m, :k], w.astype(np.int64))
     assert not D[m:].any() and not D[:, k:].any()
