@@ -42,19 +42,11 @@ namespace {
 #define WS_EXP(bit) false
 #endif
 #ifdef SI_EXPERIMENTS
-#define WS_TRACE(v)                                                                              \
-    do {                                                                                         \
-        if (X.trace && (threadIdx.x & 31) == 0) {                                                \
-            *(volatile unsigned int *)(X.trace + blockIdx.x * 64 + (threadIdx.x >> 5) * 2 + (((v) >> 27) & 1)) = (v);    \
-            __threadfence_system();                                                              \
-        }                                                                                        \
-    } while (0)
 // wait-time accounting: cycles a role spends in each of its waits (slots
 // 0..3) and in the kernel (slot 4), written per (CTA, warp) to X.stats
 #define WS_T0() const long long _t0 = clock64()
 #define WS_ACC(slot) wstat[slot] += clock64() - _t0
 #else
-#define WS_TRACE(v) ((void)0)
 #define WS_T0() ((void)0)
 #define WS_ACC(slot) ((void)0)
 #endif
@@ -64,7 +56,6 @@ enum WsExp : int32_t {
     WE_NO_MMA = 4,      // MMA warp: commits only
     WE_NO_STORE = 16,   // epilogue: no TMA stores
     WE_EPI_LDONLY = 32, // epilogue: TMEM loads + release only
-    WE_X_TILE0 = 64,    // every X load reads token tile 0 (L2-hot stream)
 };
 
 constexpr int WS_TNH = 96;                           // tokens per CTA
@@ -82,8 +73,8 @@ constexpr int WS_EPI_GROUPS = WS_EPI_WARPS / 4;
 constexpr int WS_NCH = WS_TN / 32;                   // 32-token epilogue chunks per accumulator
 constexpr int WS_NPROD = 2;                          // warps 0, 14
 constexpr int WS_PROD1_WARP = 2 + WS_EPI_WARPS;      // 14
-constexpr int WS_NGATHER = 4;                        // warps 15..18
-constexpr int WS_MMA1_WARP = 19;                     // second MMA issuer (warp 1 is the first)
+constexpr int WS_NGATHER = 2;                        // warps 15, 17
+constexpr int WS_NISSUE = 4;                         // MMA issuers: warps 1, 16, 18, 19 (one per scheduler)
 constexpr int WS_THREADS = 32 * 20;
 constexpr int WS_WSTG = 32 * 32;                     // 8-bit staging slot of one warp: 32 tokens x 32 m
 constexpr uint32_t WS_ECOL = 2 * WS_TN;              // metadata: TMEM columns 384 .. 384 + 8 * 9
@@ -93,9 +84,13 @@ static_assert(WS_TNH % 8 == 0 && WS_TN % 32 == 0 && WS_TN % 16 == 0, "tile shape
 static_assert(WS_NCH % WS_EPI_GROUPS == 0, "epilogue chunks split evenly over the column groups");
 static_assert(WS_XST % 1024 == 0 && WS_META_PER_STAGE >= 1, "ring stage");
 
+__device__ __forceinline__ int ws_issuer_index(int warp)
+{
+    return warp == 1 ? 0 : warp == 16 ? 1 : warp == 18 ? 2 : warp == 19 ? 3 : -1;
+}
 __device__ __forceinline__ int ws_gather_index(int warp)
 {
-    return warp >= 15 && warp <= 18 ? warp - 15 : -1;
+    return warp == 15 ? 0 : warp == 17 ? 1 : -1;
 }
 
 template <int OUTK>
@@ -128,7 +123,6 @@ struct WsParams {
     const uint16_t *tr_k;    // [ptiles][TR_SLOTS] activation column per residual slot (0xFFFF: unused)
     const int32_t *tr_cnt;   // [ptiles] residual MMAs (64 slots each)
     int32_t exp;             // experiment switches (WsExp; experiment builds only)
-    unsigned int *trace;     // experiment builds: per (CTA, warp) progress words in mapped host memory
     long long *stats;        // experiment builds: per (CTA, warp) wait-cycle counters (mapped host memory)
 };
 
@@ -223,48 +217,88 @@ __device__ __forceinline__ void ws_epi_tile(uint32_t lane_base, int32_t row0, in
 // together).  `q` = pairs / ptiles "main" pairs per W tile keep that tile for
 // the whole kernel and take the token tiles j, j+q, j+2q, ... below n_main;
 // the remaining H pairs split the token tiles [n_main, ntiles) of all W tiles
-// W-tile-major (at most two W loads each for H <= ptiles).  n_main balances
-// the two groups' tile counts.
-struct WsIter {
-    int pt, nt;
-    long i, i1;
-    bool ok, main;
+// W-tile-major.  n_main balances the two groups' tile counts.  A pair's work
+// is a short list of segments (one W tile, token tiles nt0, nt0+step, ... <
+// nt1): one for a main pair, one per W tile touched for a helper.
+struct WsSeg {
+    int pt, nt0, nt1, step;
 };
-__device__ __forceinline__ void ws_first(const WsParams &X, int pair, WsIter &I)
+struct WsPlan {
+    int nsegs, pt_first;
+    int nh;            // helper: token tiles per W tile in the helper region
+    int a0, a1;        // helper: first tile offset in the first segment, end offset in the last
+    bool main;
+    int j;             // main: first token tile
+};
+__device__ __forceinline__ WsPlan ws_plan(const WsParams &X, int pair)
 {
+    WsPlan W;
     const int main_pairs = X.q * X.ptiles;
-    I.main = pair < main_pairs;
-    I.i = I.i1 = 0;
-    if (I.main) {
-        I.pt = pair % X.ptiles;
-        I.nt = pair / X.ptiles;
-        I.ok = I.nt < X.n_main;
+    W.main = pair < main_pairs;
+    W.nh = X.ntiles - X.n_main;
+    W.a0 = W.a1 = W.j = 0;
+    if (W.main) {
+        W.pt_first = pair % X.ptiles;
+        W.j = pair / X.ptiles;
+        W.nsegs = W.j < X.n_main ? 1 : 0;
     } else {
-        const int nh = X.ntiles - X.n_main;
-        const long Th = (long)nh * X.ptiles;
+        const long Th = (long)W.nh * X.ptiles;
         const int h = pair - main_pairs;
-        I.i = Th * h / X.H;
-        I.i1 = Th * (h + 1) / X.H;
-        I.ok = I.i < I.i1;
-        I.pt = I.ok ? (int)(I.i / nh) : 0;
-        I.nt = I.ok ? X.n_main + (int)(I.i % nh) : 0;
-    }
-}
-__device__ __forceinline__ void ws_next(const WsParams &X, WsIter &I)
-{
-    if (I.main) {
-        I.nt += X.q;
-        I.ok = I.nt < X.n_main;
-    } else {
-        const int nh = X.ntiles - X.n_main;
-        ++I.i;
-        I.ok = I.i < I.i1;
-        if (I.ok) {
-            I.pt = (int)(I.i / nh);
-            I.nt = X.n_main + (int)(I.i % nh);
+        const long i0 = Th * h / X.H, i1 = Th * (h + 1) / X.H;
+        if (i1 <= i0) {
+            W.nsegs = 0;
+            W.pt_first = 0;
+        } else {
+            W.pt_first = (int)(i0 / W.nh);
+            const int pt_last = (int)((i1 - 1) / W.nh);
+            W.nsegs = pt_last - W.pt_first + 1;
+            W.a0 = (int)(i0 % W.nh);
+            W.a1 = (int)((i1 - 1) % W.nh) + 1;
         }
     }
+    return W;
 }
+__device__ __forceinline__ WsSeg ws_seg(const WsParams &X, const WsPlan &W, int s)
+{
+    WsSeg g;
+    if (W.main) {
+        g.pt = W.pt_first;
+        g.nt0 = W.j;
+        g.nt1 = X.n_main;
+        g.step = X.q;
+    } else {
+        g.pt = W.pt_first + s;
+        g.nt0 = X.n_main + (s == 0 ? W.a0 : 0);
+        g.nt1 = X.n_main + (s == W.nsegs - 1 ? W.a1 : W.nh);
+        g.step = 1;
+    }
+    return g;
+}
+// W tile of the tile `ahead` (1 or 2) tiles after (segment s, token tile nt), or -1
+__device__ __forceinline__ int ws_pt_ahead(const WsParams &X, const WsPlan &W, int s, const WsSeg &g, int nt, int ahead)
+{
+    int left = (g.nt1 - 1 - nt) / g.step;           // tiles after nt in this segment
+    if (ahead <= left) return g.pt;
+    ahead -= left;
+    for (int t = s + 1; t < W.nsegs; ++t) {
+        const WsSeg h = ws_seg(X, W, t);
+        const int cnt = (h.nt1 - h.nt0 + h.step - 1) / h.step;
+        if (ahead <= cnt) return h.pt;
+        ahead -= cnt;
+    }
+    return -1;
+}
+
+// Ring bookkeeping.  Iteration i of the ring (metadata iterations at a W
+// change, then kch X boxes per tile) uses stage i mod 8 in round i / 8.  The
+// ring has exactly 8 stages so that an iteration's owner is a function of its
+// stage: producer i mod 2, MMA issuer i mod 4, gather warp i mod 2.  Every
+// role therefore waits on its own stages only, round after round -- a parity
+// wait cannot tell round r from round r-2, so no role may skip a round of a
+// barrier it waits on -- and walks its iterations without a loop over the
+// others (single-warp control flow costs ~25 clk per branch: the issuers'
+// per-stage loop used to be the kernel's critical path).
+constexpr int WS_STAGES = 8;
 
 template <int MODE, int OUTK>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(WS_THREADS, 1)
@@ -273,20 +307,20 @@ k4_kernel(const __grid_constant__ CUtensorMap tmap_sa, const __grid_constant__ C
           const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_o, const K2Params P,
           const EpiParams E, const WsParams X)
 {
-    constexpr int STAGES = ws_stages<MODE, OUTK>();
-    static_assert(STAGES >= 4 && STAGES % 4 == 0, "shared memory budget / stage ownership");
+    constexpr int STAGES = WS_STAGES;
+    static_assert(ws_stages<MODE, OUTK>() >= WS_STAGES, "shared memory budget");
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t *wbuf = smem;                          // [WS_KCH + 1][8 KB] compressed A (last: residual image)
     uint8_t *rbuf = wbuf + WS_WBYTES;              // [2] gathered residual slots [96 tok x 128 slots] SW128 K-major
-    uint8_t *ring = rbuf + 2 * WS_XST;                 // [STAGES][WS_XST]
+    uint8_t *ring = rbuf + 2 * WS_XST;             // [STAGES][WS_XST]
     uint8_t *staging = ring + STAGES * WS_XST;
     uint8_t *tables = staging + ws_staged<OUTK>();
     uint16_t *glist = reinterpret_cast<uint16_t *>(tables + table_bytes<MODE>());   // [8][TR_SLOTS]
     int32_t *gcnt = reinterpret_cast<int32_t *>(glist + 8 * TR_SLOTS);              // [8]
     uint64_t *xfull = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(glist) + WS_LIST);
-    uint64_t *xpeer = xfull + STAGES;              // (peer) the stage landed: forwarded by a leader gather warp
-    uint64_t *empty = xpeer + STAGES;              // this CTA's stage: both issuers' MMAs retired + gather warps done
+    uint64_t *xpeer = xfull + STAGES;              // (peer) the stage landed: forwarded by the leader's gather warp
+    uint64_t *empty = xpeer + STAGES;              // this CTA's stage: its issuer's MMAs retired + its gather warp done
     uint64_t *tfull = empty + STAGES;              // [2]
     uint64_t *tempty = tfull + 2;                  // [2] (leader)
     uint64_t *rfull = tempty + 2;                  // [2] (leader) both CTAs' residual slots gathered
@@ -301,7 +335,6 @@ k4_kernel(const __grid_constant__ CUtensorMap tmap_sa, const __grid_constant__ C
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = tc::cluster_ctarank();
     const int pair = blockIdx.x >> 1;
-    WsIter I;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -310,16 +343,14 @@ k4_kernel(const __grid_constant__ CUtensorMap tmap_sa, const __grid_constant__ C
             tc::mbar_init(&empty[s], 2);                      // the owning issuer's commit + the owning gather warp
         }
         for (int a = 0; a < 2; ++a) {
-            tc::mbar_init(&tfull[a], 2);                      // both MMA issuers commit
+            tc::mbar_init(&tfull[a], WS_NISSUE);              // every MMA issuer commits
             tc::mbar_init(&tempty[a], 2 * WS_EPI_WARPS);
-        }
-        for (int a = 0; a < 2; ++a) {
             tc::mbar_init(&rfull[a], 2 * WS_NGATHER);
             tc::mbar_init(&rempty[a], 1);
         }
         tc::mbar_init(wfull, 1);
-        tc::mbar_init(wfree, 2);                              // both MMA issuers commit
-        tc::mbar_init(wmeta, 2);                              // both MMA issuers' metadata copies
+        tc::mbar_init(wfree, WS_NISSUE);                      // every MMA issuer commits
+        tc::mbar_init(wmeta, WS_NISSUE);                      // every MMA issuer's metadata copies
         tc::mbar_fence_init();
         tc::tma_prefetch_desc(&tmap_sa);
         tc::tma_prefetch_desc(&tmap_se);
@@ -332,82 +363,75 @@ k4_kernel(const __grid_constant__ CUtensorMap tmap_sa, const __grid_constant__ C
     tc::cluster_sync();
     tc::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const int kch = X.kchunks;
+    const int kch = X.kchunks, nmeta = X.nmeta;
+    const WsPlan Wp = ws_plan(X, pair);
 #ifdef SI_EXPERIMENTS
     long long wstat[5] = {0, 0, 0, 0, 0};
     const long long t_start = clock64();
 #endif
 
     if (warp == 0 || warp == WS_PROD1_WARP) {
-        // ---------------- TMA producers (both CTAs).  Ring iterations in
-        // order: at a W change `nmeta` metadata iterations (each stage carries
-        // up to 3 chunks' metadata tiles), then per tile `kch` X boxes.
-        // Iteration i belongs to producer i mod 2; the owner of a W change's
-        // first iteration also loads the resident A images.
+        // ---------------- TMA producers (both CTAs): producer p loads the ring
+        // iterations i = p (mod 2); both CTAs' boxes complete on the leader's
+        // barrier.  Producer 0 also loads the resident A images at a W change.
         const int prod = warp == 0 ? 0 : 1;
         const uint32_t wfull0 = tc::mapa(tc::smem_u32(wfull), 0);
-        const uint32_t xfull0 = tc::mapa(tc::smem_u32(xfull), 0);   // ring arrivals land on the leader's barriers
-        int stage = 0, wchanges = 0;
-        uint32_t phase = 0;
-        int pt_prev = -1;
-        for (ws_first(X, pair, I); I.ok; ws_next(X, I)) {
-            const int pt = I.pt, nt = I.nt;
-            if (pt != pt_prev) {
-                pt_prev = pt;
-                const int rt = 2 * pt + (int)rank;
-                if (prod == 0) {
-                    // the previous W tile's MMAs must have retired
-                    if (wchanges > 0) tc::mbar_wait(wfree, (uint32_t)(wchanges - 1) & 1);
-                    if (rank == 0) tcw::mbar_expect_tx(wfull, 2 * (kch + 1) * WS_AIMG);
-                    for (int c = 0; c < kch; ++c)
-                        tcw::tma_load_2d_2sm(wbuf + c * WS_AIMG, &tmap_sa, wfull0, 0, (rt * kch + c) * WS_IMG_ROWS);
-                    tcw::tma_load_2d_2sm(wbuf + WS_KCH * WS_AIMG, &tmap_ra, wfull0, 0, rt * WS_IMG_ROWS);
-                }
-                for (int j = 0; j < X.nmeta; ++j) {
-                    if ((stage & (WS_NPROD - 1)) == prod) {
-                        tc::mbar_wait(&empty[stage], phase ^ 1);
-                        const int c0 = j * WS_META_PER_STAGE;
-                        const int c1 = c0 + WS_META_PER_STAGE < kch + 1 ? c0 + WS_META_PER_STAGE : kch + 1;
-                        if (rank == 0) tcw::mbar_expect_tx(&xfull[stage], 2 * (c1 - c0) * WS_EIMG);
-                        for (int c = c0; c < c1; ++c) {
-                            uint8_t *dst = ring + stage * WS_XST + (c - c0) * WS_EIMG;
-                            if (c < kch)
-                                tcw::tma_load_2d_2sm(dst, &tmap_se, xfull0 + 8 * stage, 0,
-                                                     (rt * kch + c) * WS_IMG_ROWS + 64);
-                            else
-                                tcw::tma_load_2d_2sm(dst, &tmap_re, xfull0 + 8 * stage, 0, rt * WS_IMG_ROWS + 64);
-                        }
-                    }
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
-                }
-                ++wchanges;
+        const uint32_t xfull0 = tc::mapa(tc::smem_u32(xfull), 0);
+        int it = 0;
+        for (int sg = 0; sg < Wp.nsegs; ++sg) {
+            const WsSeg g = ws_seg(X, Wp, sg);
+            const int rt = 2 * g.pt + (int)rank;
+            if (prod == 0) {
+                // the previous W tile's MMAs must have retired
+                if (sg > 0) tc::mbar_wait(wfree, (uint32_t)(sg - 1) & 1);
+                if (rank == 0) tcw::mbar_expect_tx(wfull, 2 * (kch + 1) * WS_AIMG);
+                for (int c = 0; c < kch; ++c)
+                    tcw::tma_load_2d_2sm(wbuf + c * WS_AIMG, &tmap_sa, wfull0, 0, (rt * kch + c) * WS_IMG_ROWS);
+                tcw::tma_load_2d_2sm(wbuf + WS_KCH * WS_AIMG, &tmap_ra, wfull0, 0, rt * WS_IMG_ROWS);
             }
-            const int tok = (WS_EXP(WE_X_TILE0) ? 0 : nt * WS_TN) + WS_TNH * (int)rank;
-            for (int kc = 0; kc < kch; ++kc) {
-                if ((stage & (WS_NPROD - 1)) == prod) {
+            for (int j = (prod - it) & 1; j < nmeta; j += 2) {
+                const int itn = it + j, stage = itn & 7;
+                tc::mbar_wait(&empty[stage], (((uint32_t)itn >> 3) & 1) ^ 1);
+                const int c0 = j * WS_META_PER_STAGE;
+                const int c1 = c0 + WS_META_PER_STAGE < kch + 1 ? c0 + WS_META_PER_STAGE : kch + 1;
+                if (rank == 0) tcw::mbar_expect_tx(&xfull[stage], 2 * (c1 - c0) * WS_EIMG);
+                for (int c = c0; c < c1; ++c) {
+                    uint8_t *dst = ring + stage * WS_XST + (c - c0) * WS_EIMG;
+                    if (c < kch)
+                        tcw::tma_load_2d_2sm(dst, &tmap_se, xfull0 + 8 * stage, 0, (rt * kch + c) * WS_IMG_ROWS + 64);
+                    else
+                        tcw::tma_load_2d_2sm(dst, &tmap_re, xfull0 + 8 * stage, 0, rt * WS_IMG_ROWS + 64);
+                }
+            }
+            it += nmeta;
+            for (int nt = g.nt0; nt < g.nt1; nt += g.step) {
+                const int tok = nt * WS_TN + WS_TNH * (int)rank;
+                for (int kc = (prod - it) & 1; kc < kch; kc += 2) {
+                    const int itn = it + kc, stage = itn & 7;
                     {
                         WS_T0();
-                        tc::mbar_wait(&empty[stage], phase ^ 1);
+                        tc::mbar_wait(&empty[stage], (((uint32_t)itn >> 3) & 1) ^ 1);
                         WS_ACC(0);
                     }
                     if (rank == 0) tcw::mbar_expect_tx(&xfull[stage], 2 * WS_XST);
                     tcw::tma_load_2d_2sm(ring + stage * WS_XST, &tmap_x, xfull0 + 8 * stage, kc * 128, tok);
                 }
-                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                it += kch;
             }
         }
-    } else if (warp == 1 || warp == WS_MMA1_WARP) {
+    } else if (ws_issuer_index(warp) >= 0) {
         if (rank == 0) {
-            // ---------------- MMA issuers: leader CTA, two warps (one elected lane
+            // ---------------- MMA issuers: leader CTA, four warps (one elected lane
             // each issues), M256 x N192 x K64 sparse, A and metadata resident.
-            // One thread issues an MMA per ~140-180 clk whatever N is (tools/
-            // mma_rate.py), so issuer 0 takes the even 128-k stages of a tile and
-            // issuer 1 the odd ones.  Every MMA accumulates (the epilogue leaves
-            // adj[m] in the accumulator it releases), integer adds commute, so
-            // the two issue streams need no order between them; a stage, an
-            // accumulator and a W tile are complete when both issuers' commits
-            // have arrived.
-            const int mi = warp == 1 ? 0 : 1;
+            // One thread issues an MMA per ~160 clk whatever N is and its own
+            // control flow adds as much again (tools/mma_rate.py), so
+            // issuer m takes the ring iterations i = m (mod 4): at most two
+            // stages per tile, straight-line.  Every MMA accumulates (the
+            // epilogue leaves adj[m] in the accumulator it releases), integer
+            // adds commute, so the issue streams need no order between them; a
+            // stage is complete when its issuer's commit arrives, an accumulator
+            // and a W tile when all four issuers' commits have.
+            const int mi = ws_issuer_index(warp);
             const uint32_t idesc = tc::idesc_i8(256, WS_TN, 0, 0) | (1u << 2);
             const uint32_t ring_u = tc::smem_u32(ring);
             const uint64_t adesc0 = tc::smem_desc(tc::smem_u32(wbuf), 128, 512, 0);
@@ -415,21 +439,34 @@ k4_kernel(const __grid_constant__ CUtensorMap tmap_sa, const __grid_constant__ C
             const uint64_t bdesc0 = tc::smem_desc_sw128(ring_u, 16, 1024);
             const uint64_t rdesc0 = tc::smem_desc_sw128(tc::smem_u32(rbuf), 16, 1024);
             const uint32_t e_base = tmem_base + WS_ECOL;
-            int stage = 0, acc = 0, wchanges = 0, rcount = 0, pend_nres = 0, pend_acc = 0;
-            uint32_t phase = 0, acc_phase = 0;
-            int pt_prev = -1;
-            unsigned tcount = 0;
+            int it = 0, acc = 0, rcount = 0, pend_nres = 0, pend_acc = 0;
+            uint32_t acc_phase = 0;
+            // one owned X stage: wait for it, two MMAs, commit
+            auto do_stage = [&](int itn, int kc, uint32_t d_tmem) {
+                const int stage = itn & 7;
+                const uint64_t bo = bdesc0 + (uint64_t)((stage * WS_XST) >> 4);
+                const uint64_t ao = adesc0 + (uint64_t)((kc * WS_AIMG) >> 4);
+                {
+                    WS_T0();
+                    tc::mbar_spin(&xfull[stage], ((uint32_t)itn >> 3) & 1);
+                    WS_ACC(0);
+                }
+                // (TMA -> mbarrier -> MMA needs no tcgen05 fence)
+                if (!WS_EXP(WE_NO_MMA)) {
+                    tcw::mma_sp_i8_2sm(d_tmem, ao, bo, e_base + 8 * kc, idesc, 1u);
+                    tcw::mma_sp_i8_2sm(d_tmem, ao + 16, bo + 4, e_base + 8 * kc + 4, idesc, 1u);
+                }
+                tcw::mma_commit_2sm_mc(&empty[stage], 0x3);
+            };
             // (issuer 0) residual slots of the pending tile: B from the gathered
             // buffers of both CTAs, then its share of that accumulator is complete
             auto flush_residual = [&]() {
                 const int rb_sel = rcount & 1;
-                WS_TRACE(0x22000000u | ((unsigned)tcount << 8) | (unsigned)rcount);
                 {
                     WS_T0();
                     tc::mbar_spin_cluster(&rfull[rb_sel], (uint32_t)(rcount >> 1) & 1);
                     WS_ACC(2);
                 }
-                tc::tc_fence_after();
                 const uint32_t d_pend = tmem_base + pend_acc * WS_TN;
                 const uint64_t ao = adesc0 + (uint64_t)((WS_KCH * WS_AIMG) >> 4);
                 const uint64_t ro = rdesc0 + (uint64_t)((rb_sel * WS_XST) >> 4);
@@ -440,146 +477,119 @@ k4_kernel(const __grid_constant__ CUtensorMap tmap_sa, const __grid_constant__ C
                 ++rcount;
                 pend_nres = 0;
             };
-            for (ws_first(X, pair, I); I.ok; ws_next(X, I)) {
-                const int pt = I.pt;
-                if (pt != pt_prev) {
-                    pt_prev = pt;
-                    // metadata of the new W tile -> TMEM (each issuer copies the
-                    // stages it owns), once both issuers' MMAs on the previous
-                    // tile have retired; MMAs start when both issuers' copies have
-                    if (wchanges > 0) tc::mbar_spin(wfree, (uint32_t)(wchanges - 1) & 1);
-                    for (int j = 0; j < X.nmeta; ++j) {
-                        if ((stage & 1) == mi) {
-                            tc::mbar_spin(&xfull[stage], phase);
-                            tc::tc_fence_after();
-                            const uint64_t so = (uint64_t)((stage * WS_XST) >> 4);
-                            const int c0 = j * WS_META_PER_STAGE;
-                            const int c1 = c0 + WS_META_PER_STAGE < kch + 1 ? c0 + WS_META_PER_STAGE : kch + 1;
-                            for (int c = c0; c < c1; ++c)
-                                tcw::tmem_cp_128x256b_2sm(e_base + 8 * (c < kch ? c : WS_KCH),
-                                                          edesc0 + so + (uint64_t)(((c - c0) * WS_EIMG) >> 4));
-                            tcw::mma_commit_2sm_mc(&empty[stage], 0x3);
-                        }
-                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
-                    }
-                    tcw::mma_commit_2sm_mc(wmeta, 0x1);
-                    tc::mbar_spin(wmeta, (uint32_t)wchanges & 1);
-                    tc::mbar_spin(wfull, (uint32_t)wchanges & 1);
+            for (int sg = 0; sg < Wp.nsegs; ++sg) {
+                const WsSeg g = ws_seg(X, Wp, sg);
+                // metadata of the new W tile -> TMEM (each issuer copies the
+                // stages it owns), once every issuer's MMAs on the previous tile
+                // have retired; MMAs start when every issuer's copies have
+                if (sg > 0) {
+                    tc::mbar_spin(wfree, (uint32_t)(sg - 1) & 1);
                     tc::tc_fence_after();
-                    ++wchanges;
                 }
-                const int nres = __ldg(X.tr_cnt + pt);
-                WsIter Nx = I;
-                ws_next(X, Nx);
-                const bool last_of_w = !Nx.ok || Nx.pt != pt;
-                WS_TRACE(0x21000000u | ((unsigned)tcount << 8));
-                {
-                    WS_T0();
-                    tc::mbar_spin(&tempty[acc], acc_phase);      // (the epilogue's initial fill is completion 0)
-                    WS_ACC(1);
+                for (int j = (mi - it) & 3; j < nmeta; j += 4) {
+                    const int itn = it + j, stage = itn & 7;
+                    tc::mbar_spin(&xfull[stage], ((uint32_t)itn >> 3) & 1);
+                    const uint64_t so = (uint64_t)((stage * WS_XST) >> 4);
+                    const int c0 = j * WS_META_PER_STAGE;
+                    const int c1 = c0 + WS_META_PER_STAGE < kch + 1 ? c0 + WS_META_PER_STAGE : kch + 1;
+                    for (int c = c0; c < c1; ++c)
+                        tcw::tmem_cp_128x256b_2sm(e_base + 8 * (c < kch ? c : WS_KCH),
+                                                  edesc0 + so + (uint64_t)(((c - c0) * WS_EIMG) >> 4));
+                    tcw::mma_commit_2sm_mc(&empty[stage], 0x3);
                 }
+                it += nmeta;
+                tcw::mma_commit_2sm_mc(wmeta, 0x1);
+                tc::mbar_spin(wmeta, (uint32_t)sg & 1);
+                tc::mbar_spin(wfull, (uint32_t)sg & 1);
                 tc::tc_fence_after();
-                WS_TRACE(0x29000000u | ((unsigned)tcount << 8));
-                ++tcount;
-                const uint32_t d_tmem = tmem_base + acc * WS_TN;
-                for (int kc = 0; kc < kch; ++kc) {
-                    if ((stage & 1) == mi) {
-                        WS_TRACE(0x20000000u | ((unsigned)tcount << 8) | (unsigned)kc);
-                        {
-                            WS_T0();
-                            tc::mbar_spin(&xfull[stage], phase);
-                            WS_ACC(0);
-                        }
-                        tc::tc_fence_after();
-                        const uint64_t bo = bdesc0 + (uint64_t)((stage * WS_XST) >> 4);
-                        const uint64_t ao = adesc0 + (uint64_t)((kc * WS_AIMG) >> 4);
-                        if (!WS_EXP(WE_NO_MMA)) {
-                            tcw::mma_sp_i8_2sm(d_tmem, ao, bo, e_base + 8 * kc, idesc, 1u);
-                            tcw::mma_sp_i8_2sm(d_tmem, ao + 16, bo + 4, e_base + 8 * kc + 4, idesc, 1u);
-                        }
-                        tcw::mma_commit_2sm_mc(&empty[stage], 0x3);
+                const int nres = mi == 0 ? __ldg(X.tr_cnt + g.pt) : 0;
+                for (int nt = g.nt0; nt < g.nt1; nt += g.step) {
+                    {
+                        WS_T0();
+                        tc::mbar_spin(&tempty[acc], acc_phase);      // (the epilogue's initial fill is completion 0)
+                        WS_ACC(1);
                     }
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
-                    // the previous tile's residual MMAs: its last columns are
-                    // gathered only after its last stage's MMAs retired, so they
-                    // are issued a few stages into this tile (other accumulator)
-                    if (mi == 0 && pend_nres &&
-                        (kc == (kch > 2 ? 2 : kch - 1) ||
-                         tc::mbar_test_cluster(&rfull[rcount & 1], (uint32_t)(rcount >> 1) & 1)))
-                        flush_residual();
+                    tc::tc_fence_after();
+                    const uint32_t d_tmem = tmem_base + acc * WS_TN;
+                    int kc = (mi - it) & 3;
+                    if (kc < kch) do_stage(it + kc, kc, d_tmem);
+                    // the previous tile's residual MMAs (its last columns are
+                    // gathered when its last stage lands: one stage of slack)
+                    if (pend_nres) flush_residual();
+                    kc += 4;
+                    if (kc < kch) do_stage(it + kc, kc, d_tmem);
+                    it += kch;
+                    if (nres) {
+                        pend_nres = nres;
+                        pend_acc = acc;
+                        // now if the tile's slots are already gathered (the gather
+                        // runs at landing time, ahead of the MMAs), else one stage
+                        // into the next tile; the residual image leaves with the W tile
+                        if (nt + g.step >= g.nt1 ||
+                            tc::mbar_test_cluster(&rfull[rcount & 1], (uint32_t)(rcount >> 1) & 1))
+                            flush_residual();
+                    } else {
+                        tcw::mma_commit_2sm_mc(&tfull[acc], 0x3);
+                    }
+                    if (nt + g.step >= g.nt1) tcw::mma_commit_2sm_mc(wfree, 0x3);
+                    acc ^= 1;
+                    if (acc == 0) acc_phase ^= 1;
                 }
-                if (mi == 0 && nres) {
-                    pend_nres = nres;
-                    pend_acc = acc;
-                    // now if the tile's slots are already gathered, else a few stages
-                    // into the next tile; the residual image leaves with the W tile
-                    if (last_of_w || tc::mbar_test_cluster(&rfull[rcount & 1], (uint32_t)(rcount >> 1) & 1))
-                        flush_residual();
-                } else {
-                    tcw::mma_commit_2sm_mc(&tfull[acc], 0x3);
-                }
-                if (last_of_w) tcw::mma_commit_2sm_mc(wfree, 0x3);
-                acc ^= 1;
-                if (acc == 0) acc_phase ^= 1;
             }
-            if (mi == 0 && pend_nres) flush_residual();
+            if (pend_nres) flush_residual();
         }
     } else if (ws_gather_index(warp) >= 0) {
         // ---------------- residual gather (both CTAs): slot s of the residual
         // operand = activation column tr_k[s] of this CTA's tokens, copied out
         // of the streamed X box that carries it into the same SW128 layout.
         // Per W tile the slots are bucketed by 128-k chunk once (glist / gcnt).
+        // Gather warp g owns the ring iterations i = g (mod 2): it waits for
+        // the stage to land, copies all the stage's entries for the 96 tokens
+        // (lane + 32 * pass) and releases the stage.  The leader sees both
+        // CTAs' boxes complete on its barrier and forwards that to the peer.
         const int gi = ws_gather_index(warp);
-        const int gtid = gi * 32 + lane;                  // 0..127: the slot this thread files at a W change
+        const int gtid = gi * 32 + lane;
         const uint32_t rfull0 = tc::mapa(tc::smem_u32(rfull), 0);
-        // Ring stage s belongs to gather warp s mod 4: it waits for the
-        // stage to land, copies all the stage's entries for the 96 tokens (lane
-        // + 32 * pass) and releases the stage.  The leader sees both CTAs'
-        // boxes complete on its barrier; the warp owning the iteration forwards
-        // that to the peer's owner.
         const uint32_t r8 = (uint32_t)(lane & 7);
         const uint32_t rowb = (uint32_t)(lane >> 3) * 1024 + r8 * 128;
         uint64_t *landed = rank == 0 ? xfull : xpeer;
         const uint32_t xpeer1 = tc::mapa(tc::smem_u32(xpeer), 1);
-        int stage = 0, rcount = 0;
-        uint32_t phase = 0;
-        int pt_prev = -1;
-        auto stage_landed = [&]() {
+        int it = 0, rcount = 0;
+        auto stage_landed = [&](int itn) {
+            const int stage = itn & 7;
             WS_T0();
-            tc::mbar_wait_cluster(&landed[stage], phase);
+            tc::mbar_wait_cluster(&landed[stage], ((uint32_t)itn >> 3) & 1);
             WS_ACC(0);
             if (rank == 0 && lane == 0) tc::mbar_arrive_cluster(xpeer1 + 8 * stage);
         };
-        for (ws_first(X, pair, I); I.ok; ws_next(X, I)) {
-            const int pt = I.pt;
-            const int nres = __ldg(X.tr_cnt + pt);
-            if (pt != pt_prev) {
-                pt_prev = pt;
-                tc::named_bar_sync(8, 32 * WS_NGATHER);
-                if (gtid < 8) gcnt[gtid] = 0;
-                tc::named_bar_sync(8, 32 * WS_NGATHER);
-                const uint32_t k = __ldg(X.tr_k + (size_t)pt * TR_SLOTS + gtid);
-                if (gtid < 64 * nres && k != 0xFFFFu) {
+        for (int sg = 0; sg < Wp.nsegs; ++sg) {
+            const WsSeg g = ws_seg(X, Wp, sg);
+            const int nres = __ldg(X.tr_cnt + g.pt);
+            tc::named_bar_sync(8, 32 * WS_NGATHER);
+            if (gtid < 8) gcnt[gtid] = 0;
+            tc::named_bar_sync(8, 32 * WS_NGATHER);
+            for (int sl = gtid; sl < 64 * nres; sl += 32 * WS_NGATHER) {
+                const uint32_t k = __ldg(X.tr_k + (size_t)g.pt * TR_SLOTS + sl);
+                if (k != 0xFFFFu) {
                     const int c = (int)(k >> 7);
                     const int pos = atomicAdd(&gcnt[c], 1);
-                    glist[c * TR_SLOTS + pos] = (uint16_t)(((k & 127u) << 8) | (uint32_t)gtid);
-                }
-                tc::named_bar_sync(8, 32 * WS_NGATHER);
-                for (int j = 0; j < X.nmeta; ++j) {
-                    if ((stage & (WS_NGATHER - 1)) == gi) {
-                        stage_landed();
-                        __syncwarp();
-                        if (lane == 0) tc::mbar_arrive(&empty[stage]);
-                    }
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    glist[c * TR_SLOTS + pos] = (uint16_t)(((k & 127u) << 8) | (uint32_t)sl);
                 }
             }
-            const int rb_sel = rcount & 1;
-            uint8_t *rb = rbuf + rb_sel * WS_XST + rowb;
-            bool first = true;
-            for (int kc = 0; kc < kch; ++kc) {
-                if ((stage & (WS_NGATHER - 1)) == gi) {
-                    stage_landed();
+            tc::named_bar_sync(8, 32 * WS_NGATHER);
+            for (int j = (gi - it) & 1; j < nmeta; j += 2) {
+                stage_landed(it + j);
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&empty[(it + j) & 7]);
+            }
+            it += nmeta;
+            for (int nt = g.nt0; nt < g.nt1; nt += g.step) {
+                const int rb_sel = rcount & 1;
+                uint8_t *rb = rbuf + rb_sel * WS_XST + rowb;
+                bool first = true;
+                for (int kc = (gi - it) & 1; kc < kch; kc += 2) {
+                    const int itn = it + kc, stage = itn & 7;
+                    stage_landed(itn);
                     WS_T0();
                     if (nres) {
                         const int ne = gcnt[kc];
@@ -607,13 +617,13 @@ k4_kernel(const __grid_constant__ CUtensorMap tmap_sa, const __grid_constant__ C
                     WS_ACC(2);
                     if (lane == 0) tc::mbar_arrive(&empty[stage]);
                 }
-                if (++stage == STAGES) { stage = 0; phase ^= 1; }
-            }
-            if (nres) {
-                tc::fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) tc::mbar_arrive_cluster(rfull0 + 8 * rb_sel);
-                ++rcount;
+                it += kch;
+                if (nres) {
+                    tc::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) tc::mbar_arrive_cluster(rfull0 + 8 * rb_sel);
+                    ++rcount;
+                }
             }
         }
     } else if (warp >= 2 && warp < 2 + WS_EPI_WARPS) {
@@ -625,70 +635,50 @@ k4_kernel(const __grid_constant__ CUtensorMap tmap_sa, const __grid_constant__ C
         const uint32_t lane_off = (uint32_t)(W.q * 32) << 16;
         int acc = 0;
         uint32_t acc_phase = 0;
-        int pt_prev = -1;
-        WsRow k = {};
-        unsigned etile = 0;
-        (void)etile;
         // adj[m] of this lane's row in pair tile pt (the accumulators' initial value)
         auto adj_of = [&](int pt) -> int32_t {
             const int32_t m2 = pt * 256 + mrow;
-            return m2 < E.M ? __ldg(E.adj + m2) : 0;
+            return (pt >= 0 && m2 < E.M) ? __ldg(E.adj + m2) : 0;
         };
         // initial fill of both accumulators for the first two tiles, then the
         // first completion of tempty[0..1]
-        WsIter L;
-        ws_first(X, pair, L);
-        for (int a = 0; a < 2; ++a) {
-            const int32_t v = L.ok ? adj_of(L.pt) : 0;
-            for (int ch = W.g; ch < WS_NCH; ch += WS_EPI_GROUPS)
-                tc::tmem_st_32x32b_x32_fill(tmem_base + lane_off + a * WS_TN + ch * 32, (uint32_t)v);
-            if (L.ok) ws_next(X, L);
-        }
-        tc::tmem_st_wait();
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-            tc::mbar_arrive_cluster(tempty0);
-            tc::mbar_arrive_cluster(tempty0 + 8);
-        }
-        // L now runs two tiles ahead of I
-        int pt_l = -1;
-        int32_t adj_l = 0;
-        for (ws_first(X, pair, I); I.ok; ws_next(X, I)) {
-            const int pt = I.pt, nt = I.nt;
-            if (pt != pt_prev) {
-                pt_prev = pt;
-                k = ws_row<MODE>(pt * 256 + mrow, P, E);
+        if (Wp.nsegs > 0) {
+            const WsSeg g0 = ws_seg(X, Wp, 0);
+            for (int a = 0; a < 2; ++a) {
+                const int32_t v = adj_of(a == 0 ? g0.pt : ws_pt_ahead(X, Wp, 0, g0, g0.nt0, 1));
+                for (int ch = W.g; ch < WS_NCH; ch += WS_EPI_GROUPS)
+                    tc::tmem_st_32x32b_x32_fill(tmem_base + lane_off + a * WS_TN + ch * 32, (uint32_t)v);
             }
-            int32_t adj_next = 0;
-            if (L.ok) {
-                if (L.pt == pt)
-                    adj_next = k.adj;
-                else {
-                    if (L.pt != pt_l) {
-                        pt_l = L.pt;
-                        adj_l = adj_of(pt_l);
-                    }
-                    adj_next = adj_l;
+            tc::tmem_st_wait();
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                tc::mbar_arrive_cluster(tempty0);
+                tc::mbar_arrive_cluster(tempty0 + 8);
+            }
+        }
+        for (int sg = 0; sg < Wp.nsegs; ++sg) {
+            const WsSeg g = ws_seg(X, Wp, sg);
+            const WsRow k = ws_row<MODE>(g.pt * 256 + mrow, P, E);
+            for (int nt = g.nt0; nt < g.nt1; nt += g.step) {
+                // the accumulator released here next holds the tile two ahead
+                int32_t adj_next = k.adj;
+                if (nt + 2 * g.step >= g.nt1) adj_next = adj_of(ws_pt_ahead(X, Wp, sg, g, nt, 2));
+                const uint32_t te = tempty0 + 8 * acc;
+                {
+                    WS_T0();
+                    tc::mbar_wait(&tfull[acc], acc_phase);
+                    WS_ACC(0);
                 }
-                ws_next(X, L);
-            }
-            const uint32_t te = tempty0 + 8 * acc;
-            WS_TRACE(0x40000000u | (unsigned)(etile++));
-            {
+                tc::tc_fence_after();
                 WS_T0();
-                tc::mbar_wait(&tfull[acc], acc_phase);
-                WS_ACC(0);
+                ws_epi_tile<MODE, OUTK>(tmem_base + lane_off + acc * WS_TN, g.pt * 256 + 128 * (int)rank,
+                                        (int64_t)nt * WS_TN, &tmap_o, P, E, W, k, adj_next,
+                                        [te] { tc::mbar_arrive_cluster(te); }, X);
+                WS_ACC(1);
+                acc ^= 1;
+                if (acc == 0) acc_phase ^= 1;
             }
-            tc::tc_fence_after();
-            WS_TRACE(0x48000000u | (unsigned)etile);
-            WS_T0();
-            ws_epi_tile<MODE, OUTK>(tmem_base + lane_off + acc * WS_TN, pt * 256 + 128 * (int)rank,
-                                    (int64_t)nt * WS_TN, &tmap_o, P, E, W, k, adj_next,
-                                    [te] { tc::mbar_arrive_cluster(te); }, X);
-            WS_ACC(1);
-            acc ^= 1;
-            if (acc == 0) acc_phase ^= 1;
         }
         if ((OUTK == OUT_U8_W || OUTK == OUT_S8_W) && lane == 0) tc::tma_store_wait_all0();
     }
@@ -790,12 +780,9 @@ int k4_launch(const SpmmArgs &a)
     X.tr_k = img_sec<uint16_t>(a.img, h->off_tr_k);
     X.tr_cnt = img_sec<int32_t>(a.img, h->off_tr_cnt);
     X.exp = 0;
-    X.trace = nullptr;
     X.stats = nullptr;
 #ifdef SI_EXPERIMENTS
     if (const char *e = getenv("SI_WS_EXP")) X.exp = atoi(e);
-    if (const char *e = getenv("SI_WS_TRACE")) X.trace = (unsigned int *)strtoull(e, nullptr, 0);
-    X.stats = nullptr;
     if (const char *e = getenv("SI_WS_STATS")) X.stats = (long long *)strtoull(e, nullptr, 0);
 #endif
     if (h->out_dtype == SI_F32 || h->out_dtype == SI_S32) {

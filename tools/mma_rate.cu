@@ -87,14 +87,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     if ((warp == 0 || (warp == 3 && nissue == 2)) && rank == 0) {
         const int me = warp == 0 ? 0 : 1;
         uint64_t *gb = &bars[6 + 2 * me];
-        const uint32_t dacc = tb + 128 * me;
+        const uint32_t dacc = (mode & 8192) ? tb : tb + 128 * me;   // 8192: both issuers on one accumulator
         const int my_iters = iters / nissue;
         if (sparse && me == 0) tcw::tmem_cp_128x128b_2sm(tb + 384, tc::smem_desc(tc::smem_u32(sm + SM_E), 2048, 128, 0));
         uint64_t bd[4], ad[4];
         const uint64_t ed = tc::smem_desc(tc::smem_u32(sm + SM_E), 2048, 128, 0);
         for (int ks = 0; ks < 4; ++ks) {
             bd[ks] = tc::smem_desc_sw128(tc::smem_u32(sm + SM_B) + (sparse ? 64 * (ks & 1) : 32 * ks), 16, 1024);
-            if (mode & 512)        // K3's 2:4 image: SWIZZLE_NONE core matrices, LBO 128, SBO 512
+            if (mode & 16384) {    // four distinct A tiles (two 2:4 images) and B tiles (two 96-row stages)
+                ad[ks] = tc::smem_desc(tc::smem_u32(sm + SM_A) + 8192 * (ks >> 1) + 256 * (ks & 1), 128, 512, 0);
+                bd[ks] = tc::smem_desc_sw128(tc::smem_u32(sm + SM_B) + 12288 * (ks >> 1) + 64 * (ks & 1), 16, 1024);
+            } else if (mode & 512)        // K3's 2:4 image: SWIZZLE_NONE core matrices, LBO 128, SBO 512
                 ad[ks] = tc::smem_desc(tc::smem_u32(sm + SM_A) + 256 * (ks & 1), 128, 512, 0);
             else if (mode & 1024)  // SWIZZLE_64B K-major rows of 64 B
                 ad[ks] = tc::smem_desc(tc::smem_u32(sm + SM_A) + 32 * (ks & 1), 16, 512, 4);
@@ -117,7 +120,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
                         else tcw::mma_i8_2sm(dA, ad[ks], bd[ks], idesc, acc);
                     } else {
                         if (ts) mma_sp_ts_i8_2sm(dA, tb + 256 + 8 * ks, bd[ks], tb + 384, idesc, acc);
-                        else tcw::mma_sp_i8_2sm(dA, ad[ks], bd[ks], tb + 384, idesc, acc);
+                        else tcw::mma_sp_i8_2sm(dA, ad[ks], bd[ks], tb + 384 + ((mode & 32768) ? 4 * (j & 7) : 0), idesc, acc);
                     }
                     if ((mode & 128) && (j & 1)) tcw::mma_commit_2sm_mc(&bars[10], 0x3);
                 }

@@ -53,6 +53,29 @@ def main():
                                                ctypes.POINTER(ctypes.c_float), ctypes.c_int, ctypes.c_int]
     buf = torch.randint(0, 255, (32 << 20,), dtype=torch.uint8, device="cuda")
     import sys
+    if len(sys.argv) > 1 and sys.argv[1] == "ws":
+        # K4's question: sparse SS MMAs with the 2:4 image's SWIZZLE_NONE A (512),
+        # one or two issuers on ONE accumulator (4 | 8192), with and without a
+        # concurrent bulk-copy stream into shared memory
+        for N in (128, 192, 256):
+            for two in (0, 1):
+                for a_none in (0, 512):
+                    for stream in (0, 4096):
+                        mode = 2 | 16 | a_none | ((4 | 8192) if two else 0)
+                        run(L, buf, mode, N, stream, iters=1024)
+                        r = run(L, buf, mode, N, stream)
+                        extra = f"  stream {r['stream_B_clk']:5.1f} B/clk/SM" if stream else ""
+                        print(f"sparse SS N{N:3d} issuers {1 + two} A {'none' if a_none else 'sw128'}: "
+                              f"{r['cyc_per_mma']:7.1f} clk/MMA (combined){extra}", flush=True)
+        for N in (192,):
+            for extra, tag in ((128, "commit (multicast) per 2 MMAs"), (128 | 2048, "commit per 2 + busy neighbour warps"),
+                               (16384, "4 distinct A and B tiles"), (32768, "8 metadata addresses"),
+                               (16384 | 32768, "distinct A, B and metadata")):
+                mode = 2 | 16 | 512 | 4 | 8192 | extra
+                run(L, buf, mode, N, 4096, iters=1024, ld_iters=200000)
+                r = run(L, buf, mode, N, 4096, ld_iters=3000000)
+                print(f"sparse SS N{N} issuers 2, {tag}: {r['cyc_per_mma']:7.1f} clk/MMA (combined)", flush=True)
+        return
     for N, extra, tag in ((224, 16 | 64 | 128, "K3 stage pattern, idle neighbours"),
                           (224, 16 | 64 | 128 | 2048, "K3 stage, busy warps on all 4 SMSPs"),
                           (224, 16 | 64 | 128 | 4096, "K3 stage, busy warps off the issuer's SMSP")):
