@@ -1,7 +1,7 @@
 #!/bin/bash
 # One GPU call: tests, smoke, bench, reference arm, PCIe ceiling, ncu launch
 # list, ncu full captures of the dominant kernel (K2, config 5b, token-major)
-# and of the 2:4 kernel K3 on the same linear (per-variant table).  Each ncu
+# and of the 2:4 kernels K3 and K4 on the same linear (per-variant table).  Each ncu
 # step runs only after the same command exited 0 without ncu.
 set -u
 cd "${GRAFT_REPO_ROOT:-$(pwd)}"
@@ -17,7 +17,7 @@ if timeout 600 $CMD > gpurun_out/plain_launch.log 2>&1; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
      --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 fi
-for V in "top tc k2p" "sp sp k3"; do
+for V in "top tc k2p" "sp sp k3" "ws ws k4"; do
   set -- $V
   P1="python tests/prof_one.py c5b $2 3 nk"
   if timeout 300 $P1 > gpurun_out/plain_prof_$1.log 2>&1; then

@@ -43,7 +43,7 @@ def launches(tag):
     for (k, g, b), v in sorted(per.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"| `{k}` | {g} | {b} | {len(v)} | {sum(v) / len(v) / 1e3:.1f} | {sum(v) / total:.1%} |")
     lines.append("")
-    ours = sum(len(v) for (k, _, _), v in per.items() if k.startswith(("k1", "k2", "k3", "kref")))
+    ours = sum(len(v) for (k, _, _), v in per.items() if k.startswith(("k1", "k2", "k3", "k4", "kref")))
     lines.append(f"Total launches: {len(rows)}; {ours} of them are this repo's kernels, the rest are torch "
                  f"utility kernels outside the SpMM (buffer fills of the host pipeline's setup).")
     with open(os.path.join(PROF, f"{tag}_launches.md"), "w") as f:
@@ -88,8 +88,12 @@ def top(tag, cell="c5b_4096x1024", which="top", traffic_file=True):
             "derived__lts__lts2xbar_bytes.sum.per_second", "derived__lts__lts2xbar_bytes.sum.peak_sustained",
             "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
             "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+            "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+            "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
             "Kernel Name"]
-    lines = [f"# {tag}: ncu --set full of the dominant kernel ({cell}, `tests/prof_one.py c5b tc 3 nk`)", "",
+    kern = {"top": "tc", "sp": "sp", "ws": "ws"}.get(which, which)
+    what = "the dominant kernel" if which == "top" else f"kernel=\"{kern}\" on the same linear"
+    lines = [f"# {tag}: ncu --set full of {what} ({cell}, `tests/prof_one.py c5b {kern} 3 nk`)", "",
              "| metric | value |", "|---|---|"]
     for k in keys:
         if k in m:
@@ -120,6 +124,7 @@ if __name__ == "__main__":
     os.makedirs(PROF, exist_ok=True)
     launches(tag)
     top(tag)
-    if os.path.exists(os.path.join(OUT, "prof_sp_raw.csv")):
-        top(tag, which="sp", traffic_file=False)
+    for which in ("sp", "ws"):
+        if os.path.exists(os.path.join(OUT, f"prof_{which}_raw.csv")):
+            top(tag, which=which, traffic_file=False)
     print("ok")
