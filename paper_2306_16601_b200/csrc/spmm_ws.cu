@@ -78,7 +78,8 @@ constexpr int WS_NISSUE = 4;                         // MMA issuers: warps 1, 16
 constexpr int WS_THREADS = 32 * 20;
 constexpr int WS_WSTG = 32 * 32;                     // 8-bit staging slot of one warp: 32 tokens x 32 m
 constexpr uint32_t WS_ECOL = 2 * WS_TN;              // metadata: TMEM columns 384 .. 384 + 8 * 9
-constexpr int WS_LIST = 8 * TR_SLOTS * 2 + 64;       // per-chunk gather lists (u16) + counters
+constexpr int WS_LCAP = 4 * TR_SLOTS;                // gather list capacity per 128-k chunk (class-interleaved)
+constexpr int WS_LIST = 8 * WS_LCAP * 2 + 256;       // per-chunk gather lists (u16) + class counters + lengths
 static_assert(WS_ECOL + 8 * (WS_KCH + 1) <= 512, "TMEM budget");
 static_assert(WS_TNH % 8 == 0 && WS_TN % 32 == 0 && WS_TN % 16 == 0, "tile shape");
 static_assert(WS_NCH % WS_EPI_GROUPS == 0, "epilogue chunks split evenly over the column groups");
@@ -95,11 +96,14 @@ __device__ __forceinline__ int ws_gather_index(int warp)
 
 template <int OUTK>
 constexpr int ws_staged() { return (OUTK == OUT_U8_W || OUTK == OUT_S8_W) ? WS_EPI_WARPS * WS_WSTG : 0; }
+// residual B tiles: double-buffered unless the epilogue's table needs the room
+template <int MODE>
+constexpr int ws_rbufs() { return table_bytes<MODE>() ? 1 : 2; }
 template <int MODE, int OUTK>
 constexpr int ws_fixed()
 {
     // + 1024 alignment slack, 1024 barriers
-    return WS_WBYTES + 2 * WS_XST + ws_staged<OUTK>() + table_bytes<MODE>() + WS_LIST + 1024 + 1024;
+    return WS_WBYTES + ws_rbufs<MODE>() * WS_XST + ws_staged<OUTK>() + table_bytes<MODE>() + WS_LIST + 1024 + 1024;
 }
 template <int MODE, int OUTK>
 constexpr int ws_stages()
@@ -153,8 +157,10 @@ __device__ __forceinline__ WsRow ws_row(int32_t m, const K2Params &P, const EpiP
 template <int MODE, int OUTK, typename Release>
 __device__ __forceinline__ void ws_epi_tile(uint32_t lane_base, int32_t row0, int64_t tok0, const CUtensorMap *tmap_o,
                                             const K2Params &P, const EpiParams &E, EpiWarp &W, const WsRow &k,
-                                            int32_t adj_next, Release release, const WsParams &X)
+                                            int32_t adj_next, Release release, const WsParams &X,
+                                            long long *wstat = nullptr)
 {
+    (void)wstat;
     auto rel = [&]() {
         tc::tmem_st_wait();
         tc::tc_fence_before();
@@ -192,11 +198,19 @@ __device__ __forceinline__ void ws_epi_tile(uint32_t lane_base, int32_t row0, in
         const uint32_t ta = lane_base + ch * 32;
         if constexpr (STAGED) {
             // this warp's previous store must have read its staging tile
+            WS_T0();
             if (W.lane == 0) tc::tma_store_wait_read0();
             __syncwarp();
+            WS_ACC(2);
         }
+#ifdef SI_EXPERIMENTS
+        const long long t_ld = clock64();
+#endif
         // (adj is already in the accumulator: the chunk's math adds 0)
         epi_chunk<MODE, OUTK>(ta, m, mok, 0, k.s_in, cq, gm, fast, tok0 + ch * 32, 0, P, E, W, [&]() {
+#ifdef SI_EXPERIMENTS
+            wstat[3] += clock64() - t_ld;
+#endif
             tc::tmem_st_32x32b_x32_fill(ta, (uint32_t)adj_next);
             if (last) rel();
         });
@@ -313,11 +327,13 @@ k4_kernel(const __grid_constant__ CUtensorMap tmap_sa, const __grid_constant__ C
     uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t *wbuf = smem;                          // [WS_KCH + 1][8 KB] compressed A (last: residual image)
     uint8_t *rbuf = wbuf + WS_WBYTES;              // [2] gathered residual slots [96 tok x 128 slots] SW128 K-major
-    uint8_t *ring = rbuf + 2 * WS_XST;             // [STAGES][WS_XST]
+    constexpr int RB = ws_rbufs<MODE>();
+    uint8_t *ring = rbuf + RB * WS_XST;            // [STAGES][WS_XST]
     uint8_t *staging = ring + STAGES * WS_XST;
     uint8_t *tables = staging + ws_staged<OUTK>();
-    uint16_t *glist = reinterpret_cast<uint16_t *>(tables + table_bytes<MODE>());   // [8][TR_SLOTS]
-    int32_t *gcnt = reinterpret_cast<int32_t *>(glist + 8 * TR_SLOTS);              // [8]
+    uint16_t *glist = reinterpret_cast<uint16_t *>(tables + table_bytes<MODE>());   // [8][WS_LCAP]
+    int32_t *gcnt = reinterpret_cast<int32_t *>(glist + 8 * WS_LCAP);               // [8][4] entries per word class
+    int32_t *glen = gcnt + 32;                                                      // [8] list length (multiple of 4)
     uint64_t *xfull = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(glist) + WS_LIST);
     uint64_t *xpeer = xfull + STAGES;              // (peer) the stage landed: forwarded by the leader's gather warp
     uint64_t *empty = xpeer + STAGES;              // this CTA's stage: its issuer's MMAs retired + its gather warp done
@@ -461,10 +477,10 @@ k4_kernel(const __grid_constant__ CUtensorMap tmap_sa, const __grid_constant__ C
             // (issuer 0) residual slots of the pending tile: B from the gathered
             // buffers of both CTAs, then its share of that accumulator is complete
             auto flush_residual = [&]() {
-                const int rb_sel = rcount & 1;
+                const int rb_sel = rcount % RB;
                 {
                     WS_T0();
-                    tc::mbar_spin_cluster(&rfull[rb_sel], (uint32_t)(rcount >> 1) & 1);
+                    tc::mbar_spin_cluster(&rfull[rb_sel], (uint32_t)(rcount / RB) & 1);
                     WS_ACC(2);
                 }
                 const uint32_t d_pend = tmem_base + pend_acc * WS_TN;
@@ -526,7 +542,7 @@ k4_kernel(const __grid_constant__ CUtensorMap tmap_sa, const __grid_constant__ C
                         // runs at landing time, ahead of the MMAs), else one stage
                         // into the next tile; the residual image leaves with the W tile
                         if (nt + g.step >= g.nt1 ||
-                            tc::mbar_test_cluster(&rfull[rcount & 1], (uint32_t)(rcount >> 1) & 1))
+                            tc::mbar_test_cluster(&rfull[rcount % RB], (uint32_t)(rcount / RB) & 1))
                             flush_residual();
                     } else {
                         tcw::mma_commit_2sm_mc(&tfull[acc], 0x3);
@@ -542,16 +558,21 @@ k4_kernel(const __grid_constant__ CUtensorMap tmap_sa, const __grid_constant__ C
         // ---------------- residual gather (both CTAs): slot s of the residual
         // operand = activation column tr_k[s] of this CTA's tokens, copied out
         // of the streamed X box that carries it into the same SW128 layout.
-        // Per W tile the slots are bucketed by 128-k chunk once (glist / gcnt).
         // Gather warp g owns the ring iterations i = g (mod 2): it waits for
-        // the stage to land, copies all the stage's entries for the 96 tokens
-        // (lane + 32 * pass) and releases the stage.  The leader sees both
-        // CTAs' boxes complete on its barrier and forwards that to the peer.
+        // the stage to land, copies the stage's entries and releases the
+        // stage.  The leader sees both CTAs' boxes complete on its barrier and
+        // forwards that to the peer.
+        //
+        // One instruction moves 8 tokens x 4 entries (lane = 8 * entry + token):
+        // the 8 rows of a SWIZZLE_128B atom put one column into 8 different
+        // 16-byte segments, and the four entries of a quad have four different
+        // words within the segment, so the byte loads hit 32 different banks.
+        // Per W tile the slots are bucketed by 128-k chunk and word class once:
+        // list position 4 * i + c holds the i-th entry of class c (0xFFFF: none).
         const int gi = ws_gather_index(warp);
         const int gtid = gi * 32 + lane;
         const uint32_t rfull0 = tc::mapa(tc::smem_u32(rfull), 0);
-        const uint32_t r8 = (uint32_t)(lane & 7);
-        const uint32_t rowb = (uint32_t)(lane >> 3) * 1024 + r8 * 128;
+        const uint32_t r8 = (uint32_t)(lane & 7), eq = (uint32_t)(lane >> 3);
         uint64_t *landed = rank == 0 ? xfull : xpeer;
         const uint32_t xpeer1 = tc::mapa(tc::smem_u32(xpeer), 1);
         int it = 0, rcount = 0;
@@ -566,15 +587,22 @@ k4_kernel(const __grid_constant__ CUtensorMap tmap_sa, const __grid_constant__ C
             const WsSeg g = ws_seg(X, Wp, sg);
             const int nres = __ldg(X.tr_cnt + g.pt);
             tc::named_bar_sync(8, 32 * WS_NGATHER);
-            if (gtid < 8) gcnt[gtid] = 0;
+            if (gtid < 32) gcnt[gtid] = 0;
+            for (int i = gtid; i < 8 * WS_LCAP / 2; i += 32 * WS_NGATHER) reinterpret_cast<uint32_t *>(glist)[i] = 0xFFFFFFFFu;
             tc::named_bar_sync(8, 32 * WS_NGATHER);
             for (int sl = gtid; sl < 64 * nres; sl += 32 * WS_NGATHER) {
                 const uint32_t k = __ldg(X.tr_k + (size_t)g.pt * TR_SLOTS + sl);
                 if (k != 0xFFFFu) {
-                    const int c = (int)(k >> 7);
-                    const int pos = atomicAdd(&gcnt[c], 1);
-                    glist[c * TR_SLOTS + pos] = (uint16_t)(((k & 127u) << 8) | (uint32_t)sl);
+                    const int c = (int)(k >> 7), wc = (int)((k & 15u) >> 2);
+                    const int pos = atomicAdd(&gcnt[c * 4 + wc], 1);
+                    glist[c * WS_LCAP + 4 * pos + wc] = (uint16_t)(((k & 127u) << 8) | (uint32_t)sl);
                 }
+            }
+            tc::named_bar_sync(8, 32 * WS_NGATHER);
+            if (gtid < 8) {
+                int mx = 0;
+                for (int wc = 0; wc < 4; ++wc) mx = max(mx, gcnt[gtid * 4 + wc]);
+                glen[gtid] = 4 * mx;
             }
             tc::named_bar_sync(8, 32 * WS_NGATHER);
             for (int j = (gi - it) & 1; j < nmeta; j += 2) {
@@ -584,32 +612,55 @@ k4_kernel(const __grid_constant__ CUtensorMap tmap_sa, const __grid_constant__ C
             }
             it += nmeta;
             for (int nt = g.nt0; nt < g.nt1; nt += g.step) {
-                const int rb_sel = rcount & 1;
-                uint8_t *rb = rbuf + rb_sel * WS_XST + rowb;
+                const int rb_sel = rcount % RB;
+                uint8_t *rb = rbuf + rb_sel * WS_XST + r8 * 128;
                 bool first = true;
                 for (int kc = (gi - it) & 1; kc < kch; kc += 2) {
                     const int itn = it + kc, stage = itn & 7;
+                    // this lane's entries of the stage's first four quads: loaded
+                    // in the shadow of the wait for the stage
+                    const uint16_t *gl = glist + kc * WS_LCAP + eq;
+                    const int np = nres ? glen[kc] : 0;
+                    uint32_t ent[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) ent[j] = 4 * j < np ? gl[4 * j] : 0xFFFFu;
                     stage_landed(itn);
+                    if (nres && first) {
+                        // the residual MMAs two tiles back must have read this buffer
+                        WS_T0();
+                        tc::mbar_wait(&rempty[rb_sel], ((uint32_t)(rcount / RB) & 1) ^ 1);
+                        WS_ACC(1);
+                        first = false;
+                    }
                     WS_T0();
                     if (nres) {
-                        const int ne = gcnt[kc];
-                        // the residual MMAs two tiles back must have read this buffer
-                        if (first) tc::mbar_wait(&rempty[rb_sel], ((uint32_t)(rcount >> 1) & 1) ^ 1);
-                        first = false;
                         if (!WS_EXP(WE_NO_GATHER)) {
-                            const uint8_t *xs = ring + stage * WS_XST + rowb;
-                            const uint16_t *gl = glist + kc * TR_SLOTS;
-#pragma unroll 4
-                            for (int e = 0; e < ne; ++e) {
-                                const uint32_t ent = gl[e];
-                                const uint32_t ko = ent >> 8, sl = ent & 127u;
-                                const uint32_t so = (((ko >> 4) ^ r8) << 4) + (ko & 15u);
-                                const uint32_t dO = (((sl >> 4) ^ r8) << 4) + (sl & 15u);
-                                uint8_t v[WS_TNH / 32];
+                            const uint8_t *xs = ring + stage * WS_XST + r8 * 128;
+                            for (int p0 = 0; p0 < np; p0 += 16) {
+                                if (p0) {
 #pragma unroll
-                                for (int ps = 0; ps < WS_TNH / 32; ++ps) v[ps] = xs[ps * 4096 + so];
+                                    for (int j = 0; j < 4; ++j) ent[j] = p0 + 4 * j < np ? gl[p0 + 4 * j] : 0xFFFFu;
+                                }
+                                // (a missing entry reads column 0 and stores nothing)
+                                const uint8_t *src[4];
+                                uint8_t *dst[4];
+                                uint8_t v[4][WS_TNH / 8];
 #pragma unroll
-                                for (int ps = 0; ps < WS_TNH / 32; ++ps) rb[ps * 4096 + dO] = v[ps];
+                                for (int j = 0; j < 4; ++j) {
+                                    const uint32_t ko = ent[j] == 0xFFFFu ? 0u : ent[j] >> 8, sl = ent[j] & 127u;
+                                    src[j] = xs + (((ko >> 4) ^ r8) << 4) + (ko & 15u);
+                                    dst[j] = rb + (((sl >> 4) ^ r8) << 4) + (sl & 15u);
+                                }
+#pragma unroll
+                                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                                    for (int tg = 0; tg < WS_TNH / 8; ++tg) v[j][tg] = src[j][tg * 1024];
+#pragma unroll
+                                for (int j = 0; j < 4; ++j)
+                                    if (ent[j] != 0xFFFFu) {
+#pragma unroll
+                                        for (int tg = 0; tg < WS_TNH / 8; ++tg) dst[j][tg * 1024] = v[j][tg];
+                                    }
                             }
                         }
                     }
@@ -674,7 +725,11 @@ k4_kernel(const __grid_constant__ CUtensorMap tmap_sa, const __grid_constant__ C
                 WS_T0();
                 ws_epi_tile<MODE, OUTK>(tmem_base + lane_off + acc * WS_TN, g.pt * 256 + 128 * (int)rank,
                                         (int64_t)nt * WS_TN, &tmap_o, P, E, W, k, adj_next,
-                                        [te] { tc::mbar_arrive_cluster(te); }, X);
+                                        [te] { tc::mbar_arrive_cluster(te); }, X
+#ifdef SI_EXPERIMENTS
+                                        , wstat
+#endif
+                );
                 WS_ACC(1);
                 acc ^= 1;
                 if (acc == 0) acc_phase ^= 1;

@@ -25,8 +25,8 @@ s = stats.numpy().reshape(296, 20, 5).astype(np.float64)
 tot = s[:, :, 4]
 roles = {"prod0 (w0)": ([0], ["empty", "-", "-", "-"]), "prod1 (w14)": ([14], ["empty", "-", "-", "-"]),
          "mma0 (w1, leader)": ([1], ["xfull", "tempty", "kc-loop", "issue"]), "mma1-3 (w16,18,19)": ([16, 18, 19], ["xfull", "tempty", "kc-loop", "issue"]),
-         "gather (w15,17)": ([15, 17], ["landed", "-", "work+rempty", "-"]),
-         "epilogue (w2-13)": (list(range(2, 14)), ["tfull", "tile", "-", "-"])}
+         "gather (w15,17)": ([15, 17], ["landed", "rempty", "copy", "-"]),
+         "epilogue (w2-13)": (list(range(2, 14)), ["tfull", "tile", "wait_read", "tmem ld"])}
 for r, (warps, names) in roles.items():
     ctas = slice(0, 148, 2) if r.startswith("mma") else slice(0, 148)
     sel = s[ctas][:, warps, :]
