@@ -43,6 +43,10 @@ struct EpiParams {
     const int32_t *bp_key;
     const uint16_t *bp_bucket;
     int32_t bp_key_lo, bp_shift, bp_nbucket, bp_occ;
+    // linear buckets, at most one threshold each (image.h off_bp_lin); 0 entries: none
+    const uint2 *bp_lin;
+    int32_t bp_lin_n;
+    float bp_lin_inv, bp_lin_off;
 };
 
 static inline EpiParams make_epi(const SiImage *h, const void *img, const float *sides, int64_t n)
@@ -77,6 +81,10 @@ static inline EpiParams make_epi(const SiImage *h, const void *img, const float 
     e.bp_shift = h->bp_shift;
     e.bp_nbucket = h->bp_nbucket;
     e.bp_occ = h->bp_occ;
+    e.bp_lin = img_sec<uint2>(img, h->off_bp_lin);
+    e.bp_lin_n = h->bp_lin_n;
+    e.bp_lin_inv = h->bp_lin_inv;
+    e.bp_lin_off = h->bp_lin_off;
     return e;
 }
 
@@ -213,6 +221,19 @@ __device__ __forceinline__ uint32_t bp_lookup_fixed(float x, const int32_t *keys
         i = (j <= n && kk <= k) ? j : i;
     }
     return vals[i];
+}
+
+// Linear-bucket lookup (plan.cpp build_linear): the bucket function is one
+// fma, a clamp and the magic-number round-to-nearest-even; the bucket's one
+// threshold decides between its two 16-bit values.
+__device__ __forceinline__ int32_t bp_lookup_linear(float x, const uint2 *tab, float inv, float off, float nbm1)
+{
+    float t = __fmaf_rn(x, inv, off);
+    t = fminf(fmaxf(t, 0.0f), nbm1);
+    const uint32_t b = __float_as_uint(__fadd_rn(t, 8388608.0f)) & 0x7FFFFFu;
+    const uint2 e = tab[b];
+    const int32_t w = (int32_t)e.y;
+    return x >= __uint_as_float(e.x) ? (w >> 16) : ((w << 16) >> 16);
 }
 
 // _run_chain interpreter (epilogue.py:207-249) for EPI_GENERIC

@@ -15,7 +15,7 @@
 #endif
 
 #define SI_IMG_MAGIC 0x58344953u /* "SI4X" */
-#define SI_IMG_VERSION 6u   /* 6: unused residual slots carry tr_k = 0xFFFF */
+#define SI_IMG_VERSION 7u   /* 6: unused residual slots carry tr_k = 0xFFFF; 7: linear breakpoint table */
 #define TR_SLOTS 128 /* K3 residual slots per 256-row pair tile */
 
 // compiled epilogue forms (see plan.cpp: compile_program)
@@ -98,6 +98,15 @@ struct SiImage {
     uint64_t off_tr_cnt;     // i32   [pairs]             residual MMAs (64 slots each; 0..TR_SLOTS/64)
     int32_t tr_ok, tr_pairs; // tr_ok 0: some pair tile needs more than TR_SLOTS slots (K3 unavailable)
     uint64_t off_tc_wrow;    // (image v4: row-major W of the retired K2a; empty since v5)
+    // EPI_DEQ_TABLE fast path (plan.cpp build_linear): bucket b = rn(clamp(fma(x,
+    // bp_lin_inv, bp_lin_off), 0, bp_lin_n - 1)) holds at most one threshold:
+    // entry {f32 thr, i16 value below | i16 value at/above << 16}.  bp_lin_n = 0:
+    // no such table (thresholds too close, or values beyond 16 bits).
+    uint64_t off_bp_lin;     // u32x2 [bp_lin_n]
+    int32_t bp_lin_n;
+    float bp_lin_inv, bp_lin_off;
+    int32_t pad2;
+    uint64_t reserved0;
 };
 
 static_assert(sizeof(SiImage) % 16 == 0, "image header must stay 16-byte aligned");

@@ -51,6 +51,7 @@ struct K2Params {
     int32_t ntiles;      // 256-token tiles
     int32_t kchunks;     // k stages
     int32_t b_mn_major;  // 1: X is [K, N] (MN-major B), 0: [N, K] (K-major B)
+    int32_t bks;         // pair kernel: k per stage (256, or 128 for few work units per pair)
     int64_t N;
     void *out;
     int64_t ldo;
@@ -241,6 +242,13 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, i
 #pragma unroll
             for (int j = 0; j < 32; ++j) x[j] = dev_deq_acc((int32_t)(r[j] + (uint32_t)adj), s_in);
         }
+        if (E.bp_lin_n > 0) {
+            // (uniform) linear buckets with one threshold each: one compare
+            const uint2 *lin = reinterpret_cast<const uint2 *>(W.s_key);
+            const float nbm1 = (float)(E.bp_lin_n - 1);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = bp_lookup_linear(x[j], lin, E.bp_lin_inv, E.bp_lin_off, nbm1);
+        } else
         // (uniform branch on the plan's bucket occupancy) fixed-step lookups
 #define SI_BP_CHUNK(S)                                                                                          \
     for (int j = 0; j < 32; ++j)                                                                                \
@@ -408,9 +416,15 @@ __device__ __forceinline__ EpiWarp make_epi_warp(int warp, int lane, uint8_t *st
     uint16_t *s_bkt = reinterpret_cast<uint16_t *>(tables + 8 * E.n_bp + 4);
     if constexpr (MODE == EPI_DEQ_TABLE) {
         const int et = threadIdx.x - 64;
-        for (int i = et; i < E.n_bp; i += 32 * NEPI) s_key[i] = __ldg(E.bp_key + i);
-        for (int i = et; i <= E.n_bp; i += 32 * NEPI) s_val[i] = __ldg(E.bp_v + i);
-        for (int i = et; i < E.bp_nbucket; i += 32 * NEPI) s_bkt[i] = __ldg(E.bp_bucket + i);
+        if (E.bp_lin_n > 0) {
+            // the linear table (<= 2048 entries of 8 bytes) takes the whole region
+            uint2 *s_lin = reinterpret_cast<uint2 *>(tables);
+            for (int i = et; i < E.bp_lin_n; i += 32 * NEPI) s_lin[i] = __ldg(E.bp_lin + i);
+        } else {
+            for (int i = et; i < E.n_bp; i += 32 * NEPI) s_key[i] = __ldg(E.bp_key + i);
+            for (int i = et; i <= E.n_bp; i += 32 * NEPI) s_val[i] = __ldg(E.bp_v + i);
+            for (int i = et; i < E.bp_nbucket; i += 32 * NEPI) s_bkt[i] = __ldg(E.bp_bucket + i);
+        }
         tc::named_bar_sync(1 + EPI_GROUPS, 32 * NEPI);
     }
     W.s_key = s_key;

@@ -186,6 +186,9 @@ struct Compiled {
     BpTable bp;
     int32_t bp_key_lo = 0, bp_shift = 0, bp_occ = 0;
     std::vector<uint16_t> bp_bucket;
+    // linear buckets with at most one threshold each (device fast path)
+    std::vector<uint32_t> bp_lin;   // 2 words per bucket
+    float bp_lin_inv = 0, bp_lin_off = 0;
 };
 
 // Coarse index over the thresholds in f32 key space: bucket b covers keys
@@ -218,6 +221,65 @@ void build_buckets(Compiled &c)
         occ = std::max<int32_t>(occ, (int32_t)(next - c.bp_bucket[(size_t)b]));
     }
     c.bp_occ = occ;
+}
+
+// The device's bucket function (k2_common.cuh epi_chunk, EPI_DEQ_TABLE): one
+// f32 fma, a clamp and round-to-nearest-even.  It is monotone in x, so for x
+// in bucket b every threshold in a lower bucket is < x and every threshold in
+// a higher bucket is > x: with at most one threshold per bucket the piece of x
+// is decided by one compare.
+static inline int32_t lin_bucket(float x, float inv, float off, int32_t nb)
+{
+    float t = fmaf(x, inv, off);
+    t = fminf(fmaxf(t, 0.0f), (float)(nb - 1));
+    return (int32_t)nearbyintf(t);
+}
+
+// Smallest power-of-two bucket count (<= 2048: 16 KB of 8-byte entries) under
+// which no bucket holds two thresholds; values must fit 16 bits.
+void build_linear(Compiled &c)
+{
+    const size_t n = c.bp.x.size();
+    if (n == 0) return;
+    for (uint32_t v : c.bp.v) {
+        const int32_t sv = (int32_t)v;
+        if (sv < -32768 || sv > 32767) return;
+    }
+    const float lo = c.bp.x[0], hi = c.bp.x[n - 1];
+    if (!(hi > lo) && n > 1) return;
+    for (int32_t nb = 64; nb <= 2048; nb *= 2) {
+        const float inv = n > 1 ? (float)((double)(nb - 1) / ((double)hi - (double)lo)) : 0.0f;
+        const float off = -lo * inv;
+        if (!std::isfinite(inv) || !std::isfinite(off)) continue;
+        std::vector<int32_t> first((size_t)nb, -1);
+        bool ok = true;
+        int32_t prev = -1;
+        for (size_t i = 0; i < n && ok; ++i) {
+            const int32_t b = lin_bucket(c.bp.x[i], inv, off, nb);
+            ok = b > prev;            // strictly increasing: one threshold per bucket, order kept
+            prev = b;
+            if (ok) first[(size_t)b] = (int32_t)i;
+        }
+        if (!ok) continue;
+        c.bp_lin.assign((size_t)2 * nb, 0);
+        size_t before = 0;           // thresholds in lower buckets
+        for (int32_t b = 0; b < nb; ++b) {
+            float thr = INFINITY;
+            uint32_t vlo = c.bp.v[before], vhi = vlo;
+            if (first[(size_t)b] >= 0) {
+                thr = c.bp.x[(size_t)first[(size_t)b]];
+                vhi = c.bp.v[before + 1];
+                ++before;
+            }
+            uint32_t tb;
+            std::memcpy(&tb, &thr, 4);
+            c.bp_lin[(size_t)2 * b] = tb;
+            c.bp_lin[(size_t)2 * b + 1] = (vlo & 0xFFFFu) | (vhi << 16);
+        }
+        c.bp_lin_inv = inv;
+        c.bp_lin_off = off;
+        return;
+    }
 }
 
 Compiled compile_program(const si_program *p)
@@ -267,6 +329,7 @@ Compiled compile_program(const si_program *p)
             // keys + values + buckets must fit the kernels' 16 KB smem table
             if (8 * c.bp.x.size() + 4 + 2 * c.bp_bucket.size() <= 16384) {
                 c.mode = EPI_DEQ_TABLE;
+                build_linear(c);
                 return c;
             }
             c.bp = BpTable();
@@ -280,7 +343,7 @@ Compiled compile_program(const si_program *p)
 }
 
 struct Layout {
-    uint64_t off[29];
+    uint64_t off[30];
     uint64_t total;
 };
 
@@ -638,6 +701,7 @@ static Layout make_layout(const si_weight *w, const si_program *p, const Compile
     put(26, 2 * sp.tr_k.size());
     put(27, 4 * sp.tr_cnt.size());
     put(28, 0);   // (image v4: K2a row-major W, retired)
+    put(29, 4 * c.bp_lin.size());
     l.total = cur;
     return l;
 }
@@ -687,6 +751,10 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
     h->bp_shift = c.bp_shift;
     h->bp_occ = c.bp_occ;
     h->bp_nbucket = (int32_t)c.bp_bucket.size();
+    h->off_bp_lin = l.off[29];
+    h->bp_lin_n = (int32_t)(c.bp_lin.size() / 2);
+    h->bp_lin_inv = c.bp_lin_inv;
+    h->bp_lin_off = c.bp_lin_off;
     h->off_rqg = l.off[20];
     h->off_sp_img = l.off[21];
     h->off_sp_rptr = l.off[22];
@@ -811,6 +879,7 @@ extern "C" int32_t si_plan_image_build(const si_weight *w, const si_program *p, 
     } else if (!c.bp.v.empty()) {
         std::memcpy(base + h->off_bp_v, c.bp.v.data(), 4 * c.bp.v.size());
     }
+    if (!c.bp_lin.empty()) std::memcpy(base + h->off_bp_lin, c.bp_lin.data(), 4 * c.bp_lin.size());
 
     // K2 source: dense W^T [kpad][mtiles*128] int8, m contiguous
     int8_t *wt = (int8_t *)(base + h->off_tc_wt);
@@ -862,6 +931,7 @@ extern "C" int32_t si_plan_image_validate(const void *image, uint64_t bytes)
         {h->off_bp_v, 4 * ((uint64_t)h->n_bp + 1)}, {h->off_tc_wt, (uint64_t)h->tc_kpad * h->tc_mtiles * 128},
         {h->off_rqc, 4 * M}, {h->off_bp_key, 4 * (uint64_t)h->n_bp},
         {h->off_bp_bucket, 2 * (uint64_t)(h->bp_nbucket > 0 ? h->bp_nbucket : 0)}, {h->off_rqg, 4 * M},
+        {h->off_bp_lin, 8 * (uint64_t)(h->bp_lin_n > 0 ? h->bp_lin_n : 0)},
         {h->off_sp_img, rt_pad * kch * 12288}, {h->off_sp_rptr, 4 * ((uint64_t)h->tc_mtiles * 128 + 1)},
         {h->off_sp_res, 4 * (uint64_t)(h->sp_nres > 0 ? h->sp_nres : 0)}, {h->off_rqp, 4 * M},
         {h->off_tr_img, rt_pad * 12288}, {h->off_tr_k, 2 * (rt_pad / 2) * TR_SLOTS}, {h->off_tr_cnt, 4 * (rt_pad / 2)},

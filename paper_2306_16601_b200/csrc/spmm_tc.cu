@@ -175,31 +175,37 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
 }
 
 // ================================================================ CTA pair
-// Per CTA and 256-k stage: A half = 128 W rows x 256 k (32 KB), B half =
-// 128 tokens x 256 k (32 KB).
-constexpr int BKS = 256;
-constexpr int P_A = 128 * BKS;
-constexpr int P_B = 128 * BKS;
-constexpr int P_SLOT = P_A + P_B;
+// Per CTA and BKS-k stage: A half = 128 W rows x BKS k, B half = 128 tokens x
+// BKS k.  BKS = 256 (32 KB + 32 KB per stage: fewest barriers per byte, the
+// large-N default) or 128 (twice the stages in the same shared memory: a work
+// unit of few k chunks no longer fills the whole ring, so the next unit's
+// loads overlap this one's MMAs -- the small-N variant).
+template <int BKS>
+struct PairGeom {
+    static constexpr int A = 128 * BKS;
+    static constexpr int B = 128 * BKS;
+    static constexpr int SLOT = A + B;
+};
 
-template <int MODE, int OUTK>
+template <int MODE, int OUTK, int BKS>
 constexpr int pair_stages()
 {
-    constexpr int s = (SMEM_MAX - staged_bytes<OUTK>() - table_bytes<MODE>() - 2048) / P_SLOT;
+    constexpr int s = (SMEM_MAX - staged_bytes<OUTK>() - table_bytes<MODE>() - 2048) / PairGeom<BKS>::SLOT;
     return s > 8 ? 8 : s;
 }
-template <int MODE, int OUTK>
+template <int MODE, int OUTK, int BKS>
 constexpr int pair_smem()
 {
-    return pair_stages<MODE, OUTK>() * P_SLOT + staged_bytes<OUTK>() + table_bytes<MODE>() + 1024 + 512;
+    return pair_stages<MODE, OUTK, BKS>() * PairGeom<BKS>::SLOT + staged_bytes<OUTK>() + table_bytes<MODE>() + 1024 + 512;
 }
 
-template <int MODE, int OUTK>
+template <int MODE, int OUTK, int BKS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(MT_THREADS, 1)
 k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ CUtensorMap tmap_x,
            const __grid_constant__ CUtensorMap tmap_o, const K2Params P, const EpiParams E)
 {
-    constexpr int STAGES = pair_stages<MODE, OUTK>();
+    constexpr int STAGES = pair_stages<MODE, OUTK, BKS>();
+    constexpr int P_A = PairGeom<BKS>::A, P_B = PairGeom<BKS>::B, P_SLOT = PairGeom<BKS>::SLOT;
     static_assert(STAGES >= 2, "shared memory budget");
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = smem_raw + ((1024 - (tc::smem_u32(smem_raw) & 1023)) & 1023);
@@ -351,9 +357,17 @@ int launch_mode(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx,
         set_smem_attr(kern, smem);
         const int tiles = p.mtiles * p.ntiles;
         return (int)launch_pdl(kern, dim3(tiles < sms ? tiles : sms), dim3(MT_THREADS), smem, st, tw, tx, to, p, E);
+    } else if (p.bks == 128) {
+        auto kern = k2p_kernel<MODE, OUTK, 128>;
+        constexpr int smem = pair_smem<MODE, OUTK, 128>();
+        static_assert(smem <= SMEM_MAX, "shared memory budget");
+        set_smem_attr(kern, smem);
+        const int units = p.mtiles * p.ntiles;
+        const int pairs = units < sms / 2 ? units : sms / 2;
+        return (int)launch_pdl(kern, dim3(2 * pairs), dim3(MT_THREADS), smem, st, tw, tx, to, p, E);
     } else {
-        auto kern = k2p_kernel<MODE, OUTK>;
-        constexpr int smem = pair_smem<MODE, OUTK>();
+        auto kern = k2p_kernel<MODE, OUTK, 256>;
+        constexpr int smem = pair_smem<MODE, OUTK, 256>();
         static_assert(smem <= SMEM_MAX, "shared memory budget");
         set_smem_attr(kern, smem);
         const int units = p.mtiles * p.ntiles;
@@ -402,7 +416,16 @@ int k2_launch(const SpmmArgs &a)
     CUtensorMap tw, tx, to;
     const void *wt = img_sec<uint8_t>(a.img, h->off_tc_wt);
     const uint64_t mpad = (uint64_t)h->tc_mtiles * 128;
-    const uint32_t bks = single ? BK : BKS;
+    // pair kernel: 256-k stages, or 128-k stages when a pair gets only a few
+    // work units (the ring then holds more than one unit's k chunks, so the
+    // next unit's loads overlap this one's MMAs)
+    const int32_t ntiles = (int32_t)((a.n + TILE_N - 1) / TILE_N);
+    const long pair_units = (long)((h->tc_mtiles + 1) / 2) * ntiles;
+    uint32_t bks = single ? BK : (pair_units <= 6L * (num_sms() / 2) ? 128 : 256);
+#ifdef SI_EXPERIMENTS
+    if (!single)
+        if (const char *e = getenv("SI_K2_BKS")) bks = (uint32_t)atoi(e) == 128 ? 128 : 256;
+#endif
     bool ok = encode_2d(&tw, wt, mpad, (uint64_t)h->tc_kpad, mpad, 128, bks);
     if (a.layout == SI_ACT_KN)
         ok = ok && encode_2d(&tx, a.x, (uint64_t)a.n, (uint64_t)h->K, (uint64_t)a.ldx, 128, bks);
@@ -412,8 +435,9 @@ int k2_launch(const SpmmArgs &a)
     K2Params p;
     std::memset(&p, 0, sizeof(p));
     p.mtiles = single ? h->tc_mtiles : (h->tc_mtiles + 1) / 2;
-    p.ntiles = (int32_t)((a.n + TILE_N - 1) / TILE_N);
-    p.kchunks = single ? h->tc_kpad / BK : (h->tc_kpad + BKS - 1) / BKS;
+    p.ntiles = ntiles;
+    p.kchunks = single ? h->tc_kpad / BK : (h->tc_kpad + (int)bks - 1) / (int)bks;
+    p.bks = (int32_t)bks;
     p.b_mn_major = a.layout == SI_ACT_KN ? 1 : 0;
     p.N = a.n;
     p.out = a.out;

@@ -67,12 +67,14 @@ class SiImageHeader(_ct.Structure):
                 ("off_sp_rptr", _ct.c_uint64), ("off_sp_res", _ct.c_uint64), ("sp_nres", _ct.c_int32),
                 ("sp_maxres", _ct.c_int32), ("off_rqp", _ct.c_uint64), ("off_tr_img", _ct.c_uint64),
                 ("off_tr_k", _ct.c_uint64), ("off_tr_cnt", _ct.c_uint64), ("tr_ok", _ct.c_int32),
-                ("tr_pairs", _ct.c_int32), ("off_tc_wrow", _ct.c_uint64)]
+                ("tr_pairs", _ct.c_int32), ("off_tc_wrow", _ct.c_uint64), ("off_bp_lin", _ct.c_uint64),
+                ("bp_lin_n", _ct.c_int32), ("bp_lin_inv", _ct.c_float), ("bp_lin_off", _ct.c_float),
+                ("pad2", _ct.c_int32), ("reserved0", _ct.c_uint64)]
 
 
 def image_header(img: np.ndarray) -> SiImageHeader:
-    assert _ct.sizeof(SiImageHeader) == 400
-    h = SiImageHeader.from_buffer_copy(img[:400].tobytes())
+    assert _ct.sizeof(SiImageHeader) == 432
+    h = SiImageHeader.from_buffer_copy(img[:432].tobytes())
     assert h.total_bytes == img.size
     return h
 

@@ -73,3 +73,25 @@ def test_sp_unsupported_is_refused(kernel):
         K.spmm_exec(plan, K.relayout_activation(x), kernel=kernel)
     got = K.spmm_exec(plan, K.relayout_tokens(np.ascontiguousarray(x.T))).cpu().numpy()
     assert np.array_equal(got, oracle.spmm_exec(sw, x, K.raw_program(sw), bias))
+
+
+@pytest.mark.parametrize("kernel", ["sp", "ws"])
+@pytest.mark.parametrize("cell", [c for c in workloads.CONFIG5 if c.k <= 1024], ids=lambda c: c.name)
+def test_sp_config5_full(cell, kernel):
+    """BASELINE config 5 at its full size on the 2:4 kernels (the linears with
+    K <= 1024): all 65536 tokens, every output byte compared with the oracle.
+    For K4 this is also the at-scale check that several MMA issuers
+    accumulating into one tensor-memory accumulator lose no update."""
+    w, x, bias, scales = baseline_inputs(cell.m, cell.k, cell.n, cell.ratio, cell.seed)
+    sw = P.encode_sparse(w, scales)
+    prog = workloads.program(cell.program, scales)
+    plan = K.plan_spmm(sw, cell.n, program=prog, bias=bias)
+    assert _sp_applies(plan)
+    act = K.relayout_tokens(np.ascontiguousarray(x.T))
+    want = oracle.spmm_exec(sw, x, prog, bias)
+    for rep in range(2):     # a second launch right behind the first (PDL overlap)
+        got = K.spmm_exec(plan, act, kernel=kernel)
+    got = got.cpu().numpy()
+    bad = np.argwhere(got != want)
+    assert len(bad) == 0, f"{len(bad)} mismatches, first {bad[:5].tolist()}"
+

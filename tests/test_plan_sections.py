@@ -131,3 +131,39 @@ def test_k2t_residual_operand_reconstructs_weight(m, k, ratio):
         assert (trk[rt // 2, used:] == 0xFFFF).all()
     np.testing.assert_array_equal(D[:m, :k], w.astype(np.int64))
     assert not D[m:].any() and not D[:, k:].any()
+
+
+@pytest.mark.parametrize("kind", ["gelu_erf_u8", "gelu_tanh_u8"])
+def test_linear_breakpoint_table_matches_threshold_search(kind):
+    """EPI_DEQ_TABLE fast path: the linear buckets (one threshold each) give
+    the same piece as a search over the thresholds, at every threshold, a few
+    ulps either side of it, and at random points (the device's bucket function
+    restated in extended precision)."""
+    w, bias, prog, img = _plan(768, 256, 0.8, 3, kind)
+    h = image_header(img)
+    assert h.epi_mode == 4 and h.n_bp > 0
+    assert h.bp_lin_n > 0, "BASELINE's GELU -> u8 programs must get the linear table"
+    bx = image_section(img, h.off_bp_x, np.float32, h.n_bp)
+    bv = image_section(img, h.off_bp_v, np.uint32, h.n_bp + 1).astype(np.int64)
+    lin = image_section(img, h.off_bp_lin, np.uint32, 2 * h.bp_lin_n).reshape(-1, 2)
+    thr = lin[:, 0].copy().view(np.float32)
+    vlo = (lin[:, 1] & 0xFFFF).astype(np.int16).astype(np.int64)
+    vhi = (lin[:, 1] >> 16).astype(np.int16).astype(np.int64)
+    assert np.isfinite(thr).sum() == h.n_bp          # every threshold sits in its own bucket
+    xs = [bx]
+    for d in (1, 2, 3):
+        up, dn = bx.copy(), bx.copy()
+        for _ in range(d):
+            up, dn = np.nextafter(up, np.float32(np.inf)), np.nextafter(dn, np.float32(-np.inf))
+        xs += [up, dn]
+    rng = np.random.default_rng(0)
+    xs.append(rng.uniform(bx[0] - 1, bx[-1] + 1, 200000).astype(np.float32))
+    xs.append(np.array([-1e30, 1e30, 0.0, -0.0], np.float32))
+    x = np.concatenate(xs)
+    t = (x.astype(np.longdouble) * np.longdouble(np.float32(h.bp_lin_inv)) + np.longdouble(np.float32(h.bp_lin_off)))
+    t = np.clip(t.astype(np.float32), np.float32(0), np.float32(h.bp_lin_n - 1))
+    b = np.rint(t).astype(np.int64)
+    got = np.where(x >= thr[b], vhi[b], vlo[b])
+    want = bv[np.searchsorted(bx, x, side="right")].astype(np.int32).astype(np.int64)
+    bad = np.flatnonzero(got != want)
+    assert len(bad) == 0, (len(bad), x[bad[:5]], got[bad[:5]], want[bad[:5]])
