@@ -270,7 +270,7 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, i
                                                    E.bp_nbucket);
         }
 #undef SI_BP_CHUNK
-    } else if (E.mode == EPI_DEQ_SIDE) {
+    } else if constexpr (MODE == EPI_DEQ_SIDE) {
         // [DEQ_ACC, ADD_SIDE(i)] (residual connection): f32(f64(a) * f64(s))
         // + side[i][n][m] in f32, the interpreter's two steps without it
         const float *sd = E.sides + (int64_t)__ldg(E.iparams + 3) * E.N * E.M + m;

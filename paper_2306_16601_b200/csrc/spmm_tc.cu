@@ -387,6 +387,7 @@ int launch_outk(const SpmmArgs &a, const CUtensorMap &tw, const CUtensorMap &tx,
     case EPI_REQUANT: return launch_mode<EPI_REQUANT, OUTK>(a, tw, tx, to, p, single);
     case EPI_REQUANT_LUT: return launch_mode<EPI_REQUANT_LUT, OUTK>(a, tw, tx, to, p, single);
     case EPI_DEQ_TABLE: return launch_mode<EPI_DEQ_TABLE, OUTK>(a, tw, tx, to, p, single);
+    case EPI_DEQ_SIDE: return launch_mode<EPI_DEQ_SIDE, OUTK>(a, tw, tx, to, p, single);
     default: return launch_mode<EPI_GENERIC, OUTK>(a, tw, tx, to, p, single);
     }
 }

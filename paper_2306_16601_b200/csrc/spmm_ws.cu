@@ -790,6 +790,7 @@ int k4_launch_outk(const SpmmArgs &a, const CUtensorMap *tm, const K2Params &p, 
     case EPI_REQUANT: return k4_launch_mode<EPI_REQUANT, OUTK>(a, tm, p, X);
     case EPI_REQUANT_LUT: return k4_launch_mode<EPI_REQUANT_LUT, OUTK>(a, tm, p, X);
     case EPI_DEQ_TABLE: return k4_launch_mode<EPI_DEQ_TABLE, OUTK>(a, tm, p, X);
+    case EPI_DEQ_SIDE: return k4_launch_mode<EPI_DEQ_SIDE, OUTK>(a, tm, p, X);
     default: return k4_launch_mode<EPI_GENERIC, OUTK>(a, tm, p, X);
     }
 }

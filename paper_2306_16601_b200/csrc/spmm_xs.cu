@@ -530,6 +530,7 @@ int k3_launch_outk(const SpmmArgs &a, const CUtensorMap &ts, const CUtensorMap &
     case EPI_REQUANT: return k3_launch_mode<EPI_REQUANT, OUTK>(a, ts, tr, tx, to, p, X);
     case EPI_REQUANT_LUT: return k3_launch_mode<EPI_REQUANT_LUT, OUTK>(a, ts, tr, tx, to, p, X);
     case EPI_DEQ_TABLE: return k3_launch_mode<EPI_DEQ_TABLE, OUTK>(a, ts, tr, tx, to, p, X);
+    case EPI_DEQ_SIDE: return k3_launch_mode<EPI_DEQ_SIDE, OUTK>(a, ts, tr, tx, to, p, X);
     default: return k3_launch_mode<EPI_GENERIC, OUTK>(a, ts, tr, tx, to, p, X);
     }
 }
