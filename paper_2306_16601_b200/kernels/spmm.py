@@ -264,7 +264,8 @@ def spmm_exec(plan: SpmmPlan, act: ActivationLayout, pool=None, sides=None, out=
     place) or, as in the reference, a host array (numpy / CPU tensor) of shape
     [N, M] and the program's dtype: the result is computed on the GPU and
     copied into it, and ``out`` itself is returned.  ``kernel`` selects
-    "auto", "gather" (K1), "tc" (K2) or "ref"."""
+    "auto", "gather" (K1), "tc" (K2), "ref", or one of the opt-in 2:4
+    tensor-core kernels "sp" (K3) / "ws" (K4): token-major X, K <= 1024."""
     sw = plan.weight
     if act.k != sw.cols or act.n != plan.n or act.bn != plan.bn:
         raise ValueError("activation layout does not match the plan")

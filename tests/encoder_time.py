@@ -35,6 +35,22 @@ def main():
     ops = spmm_ops(cfg)
     print(f"config4 forward: {ms:.3f} ms  ({cfg.tokens / ms * 1e3:.0f} tokens/s, SpMM effective "
           f"{ops / ms / 1e9:.1f} TOPS over the whole stack)", flush=True)
+    # the same forward replayed from one CUDA graph (no host launch cost between the kernels)
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            y = enc.forward(x)
+        g.replay()
+        torch.cuda.synchronize()
+        s.record()
+        for _ in range(reps):
+            g.replay()
+        e.record()
+        torch.cuda.synchronize()
+        mg = s.elapsed_time(e) / reps
+        print(f"config4 forward, one CUDA graph: {mg:.3f} ms  ({cfg.tokens / mg * 1e3:.0f} tokens/s)", flush=True)
+    except Exception as ex:   # a forward that syncs or allocates outside torch cannot be captured
+        print("config4 forward as a CUDA graph: not capturable:", str(ex).splitlines()[0], flush=True)
     # per-op breakdown of layer 0 (eager, events around each op)
     from paper_2306_16601_b200.kernels import relayout_tokens, spmm_exec
     from paper_2306_16601_b200.kernels import eltwise as E
