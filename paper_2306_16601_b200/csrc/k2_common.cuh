@@ -36,15 +36,15 @@ __device__ __forceinline__ int producer_index(int warp, int first_extra)
 {
     return warp == 0 ? 0 : (warp >= first_extra && warp < first_extra + NPROD - 1) ? warp - first_extra + 1 : -1;
 }
-constexpr int STG_GROUP = 128 * COLS;       // staging bytes per column group (8-bit outputs)
-constexpr int STG_BYTES = EPI_GROUPS * STG_GROUP;
+constexpr int WSTG = 32 * 32;               // one per-warp staging buffer (8-bit outputs): 32 tokens x 32 m
+constexpr int STG_BYTES = EPI_WARPS * 2 * WSTG;
 constexpr int TABLE_BYTES = 16 * 1024;      // breakpoint tables staged in smem (EPI_DEQ_TABLE)
 constexpr int SMEM_MAX = 232448;
 
-// 8-bit outputs: *_TMA stage a 128-row group tile (swizzled, one TMA store
-// per column group), *_W a per-warp 32-row tile (row-major 32 B, one TMA
-// store per warp and chunk, no cross-warp barrier)
-enum OutKind { OUT_32 = 0, OUT_U8_TMA = 1, OUT_S8_TMA = 2, OUT_8_DIRECT = 3, OUT_U8_W = 4, OUT_S8_W = 5 };
+// 8-bit outputs: *_W stage a per-warp tile of 32 tokens x 32 rows (row-major
+// 32 B) and store it with one TMA store per warp and chunk (no cross-warp
+// barrier); OUT_8_DIRECT writes bytes (outputs TMA cannot address)
+enum OutKind { OUT_32 = 0, OUT_8_DIRECT = 3, OUT_U8_W = 4, OUT_S8_W = 5 };
 
 struct K2Params {
     int32_t mtiles;      // weight-row tiles (128 rows single-CTA, 256 rows per pair)
@@ -52,6 +52,7 @@ struct K2Params {
     int32_t kchunks;     // k stages
     int32_t b_mn_major;  // 1: X is [K, N] (MN-major B), 0: [N, K] (K-major B)
     int32_t bks;         // pair kernel: k per stage (256, or 128 for few work units per pair)
+    int32_t exp;         // experiment builds only (SI_K2_EXP): 1 no epilogue work, 2 no MMAs
     int64_t N;
     void *out;
     int64_t ldo;
@@ -314,23 +315,7 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, i
             else
                 word = tc::pack_sat_s8(v[4 * w + 1], v[4 * w], tc::pack_sat_s8(v[4 * w + 3], v[4 * w + 2], 0));
             word = quad_transpose(word, W.selA, W.selB);
-            *reinterpret_cast<uint32_t *>(W.stg + (4 * w + W.u) * 32 + 4 * W.i4) = word;
-        }
-    } else {
-        // saturating pack of 4 consecutive tokens, quad transpose to 4
-        // consecutive m, swizzled STS into the [token][128 m] staging tile
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-            uint32_t word;
-            if (OUTK == OUT_U8_TMA)
-                word = tc::pack_sat_u8(v[4 * w + 1], v[4 * w], tc::pack_sat_u8(v[4 * w + 3], v[4 * w + 2], 0));
-            else
-                word = tc::pack_sat_s8(v[4 * w + 1], v[4 * w], tc::pack_sat_s8(v[4 * w + 3], v[4 * w + 2], 0));
-            word = quad_transpose(word, W.selA, W.selB);
-            const int t = c * 32 + 4 * w + W.u;            // token row within the group
-            const int chunk = 2 * W.q + (W.i4 >> 2);         // 16B chunk of the 128B row
-            const int off = t * 128 + ((chunk ^ (t & 7)) << 4) + 4 * (W.i4 & 3);
-            *reinterpret_cast<uint32_t *>(W.stg + off) = word;
+            *reinterpret_cast<uint32_t *>(W.stg + c * WSTG + (4 * w + W.u) * 32 + 4 * W.i4) = word;
         }
     }
 }
@@ -344,7 +329,9 @@ __device__ __forceinline__ void epi_tile(uint32_t tmem_base, uint32_t tmem_col, 
                                          const CUtensorMap *tmap_o, const K2Params &P, const EpiParams &E,
                                          const EpiWarp &W, Wait wait_full, Release release)
 {
-    constexpr bool STAGED = (OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA);
+    // per-warp output: each warp stages its own [32 tokens][32 m] chunk (two
+    // buffers) and stores it with its own TMA store: no cross-warp barrier
+    constexpr bool PERWARP = (OUTK == OUT_U8_W || OUTK == OUT_S8_W);
     const int32_t m = row0 + W.q * 32 + W.lane;
     const bool mok = m < E.M;
     // per-row constants: issue the loads before blocking on the accumulator
@@ -359,6 +346,16 @@ __device__ __forceinline__ void epi_tile(uint32_t tmem_base, uint32_t tmem_col, 
     // gm: 1 (2: I2F conversion) when every row of the warp is proven exact
     // (no certificate), else this row's certificate guard (proven rows: 0);
     // fast: every row stays inside the magic-number range
+#ifdef SI_EXPERIMENTS
+    if (P.exp & 1) {
+        wait_full();
+        tc::tc_fence_after();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (W.lane == 0) release();
+        return;
+    }
+#endif
     const bool proven = __all_sync(0xffffffffu, gr >= 1.0f);
     const bool wide = __any_sync(0xffffffffu, gr >= 2.0f);
     const bool fast = !wide && __all_sync(0xffffffffu, gr >= 0.0f);
@@ -366,11 +363,6 @@ __device__ __forceinline__ void epi_tile(uint32_t tmem_base, uint32_t tmem_col, 
     if (proven) cq = cp;
     wait_full();
     tc::tc_fence_after();
-    if constexpr (STAGED) {
-        // the previous tile's TMA store must have finished reading the staging tile
-        if (W.q == 2 && W.lane == 0) tc::tma_store_wait_read0();
-        tc::named_bar_sync(1 + W.g, 128);
-    }
     // the accumulator is released as soon as the last chunk is in registers
     // (before its math and staging), so the MMAs of the tile after next can
     // start that much earlier
@@ -383,17 +375,22 @@ __device__ __forceinline__ void epi_tile(uint32_t tmem_base, uint32_t tmem_col, 
     for (int c = 0; c < COLS / 32; ++c) {
         const int col = W.g * COLS + c * 32;
         const uint32_t ta = tmem_base + ((uint32_t)(W.q * 32) << 16) + tmem_col + col;
+        if constexpr (PERWARP) {
+            // the store that last used this buffer (two chunks ago) has read it
+            if (W.lane == 0) tc::tma_store_wait_read1();
+            __syncwarp();
+        }
         if (c == COLS / 32 - 1)
             epi_chunk<MODE, OUTK>(ta, m, mok, adj, s_in, cq, gm, fast, tok0 + col, c, P, E, W, rel);
         else
             epi_chunk<MODE, OUTK>(ta, m, mok, adj, s_in, cq, gm, fast, tok0 + col, c, P, E, W);
-    }
-    if constexpr (STAGED) {
-        tc::fence_proxy_async_smem();
-        tc::named_bar_sync(1 + W.g, 128);
-        if (W.q == 2 && W.lane == 0) {
-            tc::tma_store_2d(tmap_o, W.stg, row0, (int32_t)(tok0 + W.g * COLS));
-            tc::tma_store_commit();
+        if constexpr (PERWARP) {
+            tc::fence_proxy_async_smem();
+            __syncwarp();
+            if (W.lane == 0) {
+                tc::tma_store_2d(tmap_o, W.stg + c * WSTG, row0 + W.q * 32, (int32_t)(tok0 + col));
+                tc::tma_store_commit();
+            }
         }
     }
 }
@@ -410,7 +407,7 @@ __device__ __forceinline__ EpiWarp make_epi_warp(int warp, int lane, uint8_t *st
     W.i4 = lane >> 2;
     W.selA = (W.u & 1) ? 0x3715u : 0x6240u;
     W.selB = (W.u & 2) ? 0x3276u : 0x5410u;
-    W.stg = staging + W.g * STG_GROUP;
+    W.stg = staging + (warp - 2) * (2 * WSTG);   // this warp's two [32 tokens][32 m] staging buffers
     int32_t *s_key = reinterpret_cast<int32_t *>(tables);
     uint32_t *s_val = reinterpret_cast<uint32_t *>(tables + 4 * E.n_bp);
     uint16_t *s_bkt = reinterpret_cast<uint16_t *>(tables + 8 * E.n_bp + 4);
@@ -434,7 +431,7 @@ __device__ __forceinline__ EpiWarp make_epi_warp(int warp, int lane, uint8_t *st
 }
 
 template <int OUTK>
-constexpr int staged_bytes() { return (OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA) ? STG_BYTES : 0; }
+constexpr int staged_bytes() { return (OUTK == OUT_32 || OUTK == OUT_8_DIRECT) ? 0 : STG_BYTES; }
 template <int MODE>
 constexpr int table_bytes() { return MODE == EPI_DEQ_TABLE ? TABLE_BYTES : 0; }
 

@@ -24,8 +24,8 @@
 // Epilogue (all compiled forms of the reference's _run_chain,
 // epilogue.py:207-249; k2_common.cuh): tcgen05.ld 32x32b.x32 -> registers ->
 // the form's math -> 8-bit outputs: saturating pack, 4x4 quad byte
-// transpose, 128B-swizzled smem tile, TMA store; 32-bit outputs: coalesced
-// 128-byte rows.  The requant form (BASELINE config 5) uses the plan's proven
+// transpose, a per-warp [32 tokens][32 m] smem tile, one TMA store per warp
+// and chunk; 32-bit outputs: coalesced 128-byte rows.  The requant form (BASELINE config 5) uses the plan's proven
 // per-row multipliers (one fma onto the magic number 1.5*2^23 + zp) or the
 // f32 certificate path with an exact f64 fallback (k2_common.cuh epi_chunk).
 #include "k2_common.cuh"
@@ -106,7 +106,7 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                         continue;
                     }
-                    tc::mbar_spin(&empty[stage], phase ^ 1);
+                    tc::mbar_wait(&empty[stage], phase ^ 1);   // (try_wait: no polling traffic on the shared-memory pipe)
                     uint8_t *a_s = smem + stage * S_STAGE;
                     uint8_t *b_s = a_s + S_A;
                     tc::mbar_expect_tx(&full[stage], S_STAGE);
@@ -164,7 +164,7 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
-        if ((OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA) && W.q == 2 && lane == 0) tc::tma_store_wait_all0();
+        if ((OUTK == OUT_U8_W || OUTK == OUT_S8_W) && lane == 0) tc::tma_store_wait_all0();
     }
     tc::tc_fence_before();
     __syncthreads();
@@ -263,7 +263,7 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                         continue;
                     }
-                    tc::mbar_spin(&empty[stage], phase ^ 1);
+                    tc::mbar_wait(&empty[stage], phase ^ 1);   // (try_wait: no polling traffic on the shared-memory pipe)
                     uint8_t *a_s = ring + stage * P_SLOT;
                     const uint32_t fb = full0 + 8 * stage;
                     if (rank == 0) tcw::mbar_expect_tx(&full[stage], 2 * P_SLOT);
@@ -297,6 +297,10 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
                     tc::mbar_spin(&full[stage], phase);
                     tc::tc_fence_after();
                     const uint64_t so = (uint64_t)((stage * P_SLOT) >> 4);
+#ifdef SI_EXPERIMENTS
+                    if (P.exp & 2) {
+                    } else
+#endif
                     if (P.b_mn_major) {
 #pragma unroll
                         for (int kk = 0; kk < BKS / 32; ++kk)
@@ -333,7 +337,7 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
         }
-        if ((OUTK == OUT_U8_TMA || OUTK == OUT_S8_TMA) && W.q == 2 && lane == 0) tc::tma_store_wait_all0();
+        if ((OUTK == OUT_U8_W || OUTK == OUT_S8_W) && lane == 0) tc::tma_store_wait_all0();
     }
     tc::tc_fence_before();
     tc::cluster_sync();
@@ -439,6 +443,9 @@ int k2_launch(const SpmmArgs &a)
     p.ntiles = ntiles;
     p.kchunks = single ? h->tc_kpad / BK : (h->tc_kpad + (int)bks - 1) / (int)bks;
     p.bks = (int32_t)bks;
+#ifdef SI_EXPERIMENTS
+    if (const char *e = getenv("SI_K2_EXP")) p.exp = atoi(e);
+#endif
     p.b_mn_major = a.layout == SI_ACT_KN ? 1 : 0;
     p.N = a.n;
     p.out = a.out;
@@ -450,13 +457,17 @@ int k2_launch(const SpmmArgs &a)
         std::memset(&to, 0, sizeof(to));
         return launch_outk<OUT_32>(a, tw, tx, to, p, single);
     }
-    // 8-bit outputs: TMA store of a swizzled smem tile
+    // 8-bit outputs: every epilogue warp stages its own [32 tokens][32 m]
+    // chunk and TMA-stores it as a 32 x 32 box (no cross-warp barrier on the
+    // output path: 1-4% faster than one swizzled 128-row tile per column
+    // group, profiles/r02_k2_experiments.md)
     const bool tma_ok = (a.ldo % 16 == 0) && ((uintptr_t)a.out % 16 == 0) &&
-                        encode_2d(&to, a.out, (uint64_t)h->M, (uint64_t)a.n, (uint64_t)a.ldo, 128, COLS);
+                        encode_2d(&to, a.out, (uint64_t)h->M, (uint64_t)a.n, (uint64_t)a.ldo, 32, 32,
+                                  CU_TENSOR_MAP_SWIZZLE_NONE);
     if (!tma_ok) {
         std::memset(&to, 0, sizeof(to));
         return launch_outk<OUT_8_DIRECT>(a, tw, tx, to, p, single);
     }
-    return h->out_dtype == SI_U8 ? launch_outk<OUT_U8_TMA>(a, tw, tx, to, p, single)
-                                 : launch_outk<OUT_S8_TMA>(a, tw, tx, to, p, single);
+    return h->out_dtype == SI_U8 ? launch_outk<OUT_U8_W>(a, tw, tx, to, p, single)
+                                 : launch_outk<OUT_S8_W>(a, tw, tx, to, p, single);
 }
