@@ -16,3 +16,11 @@ for sparse in (0, 2):
             r = M.run(L, buf, mode, N, stream)
             extra = f"  stream {r['stream_B_clk']:5.1f} B/clk/SM" if stream else ""
             print(f"{'sparse' if sparse else 'dense'} SS N{N} issuers {1+two}: {r['cyc_per_mma']:7.1f} clk/MMA  {r['mac_clk_sm']:7.0f} MAC/clk/SM{extra}", flush=True)
+print("--- sustained: dense SS N256, 2 issuers, stream; SM clock = cycles / globaltimer")
+for iters in (8192, 65536, 524288):
+    mode = 0 | 16 | 4 | 8192
+    out = (ctypes.c_ulonglong * (148 * 4))()
+    ms = ctypes.c_float()
+    err = L.mma_rate(mode, iters, 256, 4096, 148, ctypes.c_void_p(buf.data_ptr()), buf.numel() // 16384, out, ctypes.byref(ms), 0, 0)
+    cyc = out[0]; ns = out[1]
+    print(f"iters {iters}: {cyc/iters:.1f} clk/MMA, {ns/1e3:.0f} us, SM clock {cyc/ns*1e3:.0f} MHz, rc {err}", flush=True)
