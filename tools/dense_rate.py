@@ -1,3 +1,9 @@
+"""Dense / sparse tcgen05 kind::i8 MMA rate with one and two issuers, and the SM clock
+under a sustained MMA load (clock64 / %globaltimer), on the GPU box:
+
+    python tools/dense_rate.py
+
+Uses the microbenchmark kernel of tools/mma_rate.cu (profiles/r02_k2_experiments.md, section 2)."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import ctypes, torch
