@@ -62,27 +62,34 @@ def main():
         ev = torch.cuda.Event(enable_timing=True)
         ev.record()
         marks.append((name, ev))
-    mark("start")
-    xq = E.quantize_f32(x, q.qp_in); mark("quantize in")
-    qkv = spmm_exec(L.plans["qkv"], relayout_tokens(xq)); mark("spmm qkv 2304x768")
-    # attention, op by op (the composition of BertEncoder._attention)
-    B, S, H, nh = cfg.batch, cfg.seq, cfg.hidden, cfg.heads
-    d, ld = H // nh, 3 * H
-    scores = torch.empty((B, nh, S, S), dtype=torch.float32, device="cuda")
-    E.bmm_strided(qkv, qkv[:, H:], scores, B, nh, S, d, S, (S * ld, d, ld), (S * ld, d, ld),
-                  (nh * S * S, S * S, S), True, E.attention_scale(d)); mark("  scores bmm (NT)")
-    E.softmax_f32(scores, out=scores); mark("  softmax")
-    ctx = torch.empty((B * S, H), dtype=torch.float32, device="cuda")
-    E.bmm_strided(scores, qkv[:, 2 * H:], ctx, B, nh, S, S, d, (nh * S * S, S * S, S), (S * ld, d, ld),
-                  (S * H, d, H), False, 1.0); mark("  context bmm (NN)")
-    E.attention_fused(qkv, ctx, B, S, nh, d, E.attention_scale(d)); mark("  attention fused (same result)")
-    cq = E.quantize_f32(ctx, q.qp_ctx); mark("quantize ctx")
-    a = spmm_exec(L.plans["o"], relayout_tokens(cq), sides=x.view(1, cfg.tokens, cfg.hidden)); mark("spmm o +res")
-    h1 = E.layer_norm_f32(a, L.gamma1, L.beta1, cfg.eps); mark("layer norm 1")
-    h1q = E.quantize_f32(h1, q.qp_h1); mark("quantize h1")
-    f = spmm_exec(L.plans["ffn1"], relayout_tokens(h1q)); mark("spmm ffn1 +gelu+quant")
-    g = spmm_exec(L.plans["ffn2"], relayout_tokens(f), sides=h1.view(1, cfg.tokens, cfg.hidden)); mark("spmm ffn2 +res")
-    E.layer_norm_f32(g, L.gamma2, L.beta2, cfg.eps); mark("layer norm 2")
+    def one_pass():
+        mark("start")
+        xq = E.quantize_f32(x, q.qp_in); mark("quantize in")
+        qkv = spmm_exec(L.plans["qkv"], relayout_tokens(xq)); mark("spmm qkv 2304x768")
+        # attention, op by op (the composition of BertEncoder._attention)
+        B, S, H, nh = cfg.batch, cfg.seq, cfg.hidden, cfg.heads
+        d, ld = H // nh, 3 * H
+        scores = torch.empty((B, nh, S, S), dtype=torch.float32, device="cuda")
+        E.bmm_strided(qkv, qkv[:, H:], scores, B, nh, S, d, S, (S * ld, d, ld), (S * ld, d, ld),
+                      (nh * S * S, S * S, S), True, E.attention_scale(d)); mark("  scores bmm (NT)")
+        E.softmax_f32(scores, out=scores); mark("  softmax")
+        ctx = torch.empty((B * S, H), dtype=torch.float32, device="cuda")
+        E.bmm_strided(scores, qkv[:, 2 * H:], ctx, B, nh, S, S, d, (nh * S * S, S * S, S), (S * ld, d, ld),
+                      (S * H, d, H), False, 1.0); mark("  context bmm (NN)")
+        E.attention_fused(qkv, ctx, B, S, nh, d, E.attention_scale(d)); mark("  attention fused (same result)")
+        cq = E.quantize_f32(ctx, q.qp_ctx); mark("quantize ctx")
+        a = spmm_exec(L.plans["o"], relayout_tokens(cq), sides=x.view(1, cfg.tokens, cfg.hidden)); mark("spmm o +res")
+        h1 = E.layer_norm_f32(a, L.gamma1, L.beta1, cfg.eps); mark("layer norm 1")
+        h1q = E.quantize_f32(h1, q.qp_h1); mark("quantize h1")
+        f = spmm_exec(L.plans["ffn1"], relayout_tokens(h1q)); mark("spmm ffn1 +gelu+quant")
+        g = spmm_exec(L.plans["ffn2"], relayout_tokens(f), sides=h1.view(1, cfg.tokens, cfg.hidden)); mark("spmm ffn2 +res")
+        E.layer_norm_f32(g, L.gamma2, L.beta2, cfg.eps); mark("layer norm 2")
+
+    # two passes: the first one pays the allocator and first-launch costs, the second is reported
+    one_pass()
+    torch.cuda.synchronize()
+    marks.clear()
+    one_pass()
     torch.cuda.synchronize()
     for (n0, e0), (n1, e1) in zip(marks, marks[1:]):
         print(f"  {n1:32s} {e0.elapsed_time(e1) * 1e3:8.1f} us", flush=True)
