@@ -16,6 +16,11 @@
 //       D[256 W rows x 256 tokens] per tile with 256-k stages; each CTA holds
 //       half of A and half of B, so every SM moves half the operand bytes.
 //
+// Every single-thread role waits with mbarrier.try_wait (the hardware
+// suspends the warp) rather than a test_wait polling loop: the kernel is
+// power-limited (profiles/r02_k2_experiments.md), and the polling warps cost
+// 0.3-0.5% of every config-5 linear.
+//
 // Roles: warp 0 and warps 18-19 TMA producers, warp 1 TMEM allocator + MMA
 // issuer (one elected lane; in a pair only the leader CTA issues), warps
 // 2-17 the epilogue (4 per TMEM lane quarter, 64 tokens each).  TMEM holds
@@ -127,11 +132,11 @@ k2_tc_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
             for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-                tc::mbar_spin(&tempty[acc], acc_phase ^ 1);
+                tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * TILE_N;
                 for (int kc = 0; kc < P.kchunks; ++kc) {
-                    tc::mbar_spin(&full[stage], phase);
+                    tc::mbar_wait(&full[stage], phase);
                     tc::tc_fence_after();
                     const uint32_t a_addr = tc::smem_u32(smem + stage * S_STAGE);
                     const uint32_t b_addr = a_addr + S_A;
@@ -290,11 +295,11 @@ k2p_kernel(const __grid_constant__ CUtensorMap tmap_w, const __grid_constant__ C
             int stage = 0, acc = 0;
             uint32_t phase = 0, acc_phase = 0;
             for (int unit = pair; unit < units; unit += npairs) {
-                tc::mbar_spin(&tempty[acc], acc_phase ^ 1);
+                tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * TILE_N;
                 for (int kc = 0; kc < P.kchunks; ++kc) {
-                    tc::mbar_spin(&full[stage], phase);
+                    tc::mbar_wait(&full[stage], phase);
                     tc::tc_fence_after();
                     const uint64_t so = (uint64_t)((stage * P_SLOT) >> 4);
 #ifdef SI_EXPERIMENTS
