@@ -13,9 +13,13 @@
 // the reference, and is order independent, so any schedule gives the same
 // bits.  The epilogue runs in registers; a CTA (8 warps = 32 output rows)
 // stages its [128 tokens x 32 rows] tile in shared memory and writes it out
-// token-major ([N, M], spmm.py:236) with coalesced row segments.
+// token-major ([N, M], spmm.py:236) with coalesced row segments.  K1s (below)
+// is the same kernel reading its gathered rows from a cp.async-staged slab.
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <mutex>
+#include <set>
 
 #include "epilogue.cuh"
 #include "si_internal.h"
@@ -119,6 +123,110 @@ k1_gather_kernel(const int32_t *__restrict__ tile_ptr, const uint4 *__restrict__
     }
 }
 
+// K1s: the same kernel with the CTA's activation tile staged in shared memory.
+// The whole [K x 128 tokens] slab the CTA's 8 groups gather from is brought in
+// once with 16-byte cp.async (K * 128 B <= K1S_SMEM), so the gathered row
+// loads of the block loop are conflict-free LDS.32 instead of dependent L2
+// round trips (the small-N cells are latency-bound: 24 CTAs of config 1 each
+// walk ~20 micro-tiles).  Needs [K, N] activations with a 16-byte-aligned
+// base and leading dimension (the transposed workspace of the [N, K] path
+// qualifies); everything after the block loop is K1's.
+constexpr int K1S_SMEM = 200 * 1024;
+
+__device__ __forceinline__ void cp_async_16(uint32_t dst, const void *src)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+
+template <int MODE, int OUTB>
+__global__ void __launch_bounds__(K1_WARPS * 32)
+k1s_gather_kernel(const int32_t *__restrict__ tile_ptr, const uint4 *__restrict__ tile_w,
+                  const int4 *__restrict__ tile_idx, int32_t groups, int32_t K, const uint8_t *__restrict__ x,
+                  int64_t ldx, int64_t N, void *__restrict__ out, int64_t ldo, EpiParams E)
+{
+    extern __shared__ __align__(16) uint8_t xs[];          // [K][K1_TOK]
+    __shared__ uint32_t stage[K1_ROWS][K1_TOK + 1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int32_t g = blockIdx.y * K1_WARPS + warp;
+    const int64_t nb = (int64_t)blockIdx.x * K1_TOK;
+    const int64_t n0 = nb + lane * 4;
+    // weights of this warp's first micro-tiles do not depend on the previous kernel
+    int32_t t0 = 0, t1 = 0;
+    if (g < groups) {
+        t0 = __ldg(tile_ptr + g);
+        t1 = __ldg(tile_ptr + g + 1);
+    }
+    SI_PDL_ENTRY();
+    {
+        // stage the slab: 8 chunks of 16 B per activation row (chunks wholly
+        // past the leading dimension are skipped; their tokens are never stored)
+        const uint32_t xs_u = (uint32_t)__cvta_generic_to_shared(xs);
+        const int chunks = K * (K1_TOK / 16);
+        for (int c = threadIdx.x; c < chunks; c += K1_WARPS * 32) {
+            const int k = c >> 3, j = c & 7;
+            const int64_t col = nb + 16 * j;
+            if (col < ldx) cp_async_16(xs_u + (uint32_t)c * 16, x + (int64_t)k * ldx + col);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+    }
+
+    int32_t acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) acc[r][t] = 0;
+
+    if (g < groups) {
+        const uint32_t *xw = reinterpret_cast<const uint32_t *>(xs) + lane;   // this lane's 4 tokens of row 0
+#pragma unroll 4
+        for (int32_t t = t0; t < t1; ++t) {
+            const uint4 w = __ldg(tile_w + t);
+            const int4 ix = __ldg(tile_idx + t);
+            const uint32_t x0 = xw[ix.x * (K1_TOK / 4)], x1 = xw[ix.y * (K1_TOK / 4)];
+            const uint32_t x2 = xw[ix.z * (K1_TOK / 4)], x3 = xw[ix.w * (K1_TOK / 4)];
+            const uint32_t lo01 = __byte_perm(x0, x1, 0x5140), lo23 = __byte_perm(x2, x3, 0x5140);
+            const uint32_t hi01 = __byte_perm(x0, x1, 0x7362), hi23 = __byte_perm(x2, x3, 0x7362);
+            const uint32_t tok[4] = {__byte_perm(lo01, lo23, 0x5410), __byte_perm(lo01, lo23, 0x7632),
+                                     __byte_perm(hi01, hi23, 0x5410), __byte_perm(hi01, hi23, 0x7632)};
+            const uint32_t wr[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int tt = 0; tt < 4; ++tt) acc[r][tt] = dp4a_us(tok[tt], wr[r], acc[r][tt]);
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int32_t m = g * 4 + r;
+            if (m < E.M) {
+                const int32_t adj = __ldg(E.adj + m);
+#pragma unroll
+                for (int tt = 0; tt < 4; ++tt) {
+                    const int64_t n = n0 + tt;
+                    uint32_t v = 0;
+                    if (n < N) v = epi_apply<MODE>((int32_t)((uint32_t)acc[r][tt] + (uint32_t)adj), m, n, E);
+                    stage[warp * 4 + r][lane * 4 + tt] = v;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const int32_t m0 = blockIdx.y * K1_ROWS;
+    const int32_t mrow = m0 + lane;
+    for (int t = warp; t < K1_TOK; t += K1_WARPS) {
+        const int64_t n = nb + t;
+        if (n >= N) break;
+        if (mrow < E.M) {
+            const uint32_t v = stage[lane][t];
+            if (OUTB == 4)
+                reinterpret_cast<uint32_t *>(out)[n * ldo + mrow] = v;
+            else
+                reinterpret_cast<uint8_t *>(out)[n * ldo + mrow] = (uint8_t)(v & 0xFF);
+        }
+    }
+}
+
 // [N, K] token-major -> [K, ldt] (ldt = N rounded up to 16) through smem
 __global__ void transpose_nk_kernel(const uint8_t *__restrict__ x, int64_t ldx, int64_t N, int32_t K,
                                     uint8_t *__restrict__ xt, int64_t ldt)
@@ -180,6 +288,23 @@ void launch_k1_mode(const SpmmArgs &a, const uint8_t *x, int64_t ldx, bool vec, 
     auto tp = img_sec<int32_t>(a.img, h->off_tile_ptr);
     auto tw = img_sec<uint4>(a.img, h->off_tile_w);
     auto ti = img_sec<int4>(a.img, h->off_tile_idx);
+    // staged variant: 16-byte-aligned [K, N] activations whose slab fits
+    const size_t slab = (size_t)h->K * K1_TOK;
+    if (ldx % 16 == 0 && ((uintptr_t)x) % 16 == 0 && slab <= (size_t)K1S_SMEM) {
+        auto kern = k1s_gather_kernel<MODE, OUTB>;
+        static std::mutex mu;
+        static std::set<int> done;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            if (done.insert(dev).second)
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K1S_SMEM);
+        }
+        launch_pdl(kern, dim3(grid), dim3(K1_WARPS * 32), slab, st, tp, tw, ti, h->groups, h->K, x, ldx, a.n, a.out,
+                   a.ldo, E);
+        return;
+    }
     if (vec)
         launch_pdl(k1_gather_kernel<MODE, OUTB, true>, dim3(grid), dim3(K1_WARPS * 32), 0, st, tp, tw, ti, h->groups, x, ldx, a.n,
                                                                           a.out, a.ldo, E);
