@@ -30,6 +30,9 @@ int32_t pick_kernel(const SiImage *h, int64_t n, int32_t layout, int32_t kernel,
                     int64_t ldo)
 {
     if (kernel != SI_KERNEL_AUTO) return kernel;
+    // one wave of the staged gather kernel on a very sparse weight beats the
+    // tensor-core kernel's fixed cost (small N, >= 85-90% sparsity)
+    if (k1s_preferred(h, n, layout, x, ldx)) return SI_KERNEL_GATHER;
     // tensor cores whenever TMA-legal, except tiny weights at small N where
     // the gather kernel's single wave is shorter (all 140 config-2 cells,
     // CUDA-graph replay: profiles/r01b_config2_*.md, DESIGN.md "Kernel

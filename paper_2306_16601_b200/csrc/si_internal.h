@@ -56,6 +56,9 @@ struct SpmmArgs {
 
 // K1: CUDA-core gather (spmm_gather.cu).  Returns a cudaError_t value.
 int k1_launch(const SpmmArgs &a);
+// AUTO: the staged gather kernel (K1s) is the faster one for this call (one
+// wave of CTAs, few blocks per group; measured crossover)
+bool k1s_preferred(const SiImage *h, int64_t n, int32_t layout, const void *x, int64_t ldx);
 uint64_t k1_workspace(const SiImage *h, int64_t n, int32_t layout);
 int k1_launch_count(const SiImage *h, int32_t layout);
 

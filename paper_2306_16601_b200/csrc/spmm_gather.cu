@@ -125,13 +125,16 @@ k1_gather_kernel(const int32_t *__restrict__ tile_ptr, const uint4 *__restrict__
 
 // K1s: the same kernel with the CTA's activation tile staged in shared memory.
 // The whole [K x 128 tokens] slab the CTA's 8 groups gather from is brought in
-// once with 16-byte cp.async (K * 128 B <= K1S_SMEM), so the gathered row
+// once with 16-byte cp.async (K * 128 B <= K1S_SLAB), and each warp's first
+// K1S_TILES micro-tiles (weights + column indices) with it, so the gathered row
 // loads of the block loop are conflict-free LDS.32 instead of dependent L2
 // round trips (the small-N cells are latency-bound: 24 CTAs of config 1 each
 // walk ~20 micro-tiles).  Needs [K, N] activations with a 16-byte-aligned
 // base and leading dimension (the transposed workspace of the [N, K] path
 // qualifies); everything after the block loop is K1's.
-constexpr int K1S_SMEM = 200 * 1024;
+constexpr int K1S_TILES = 128;                        // micro-tiles per group staged next to the slab
+constexpr int K1S_WBYTES = K1_WARPS * K1S_TILES * 32; // their weights + column indices (32 KB)
+constexpr int K1S_SLAB = 160 * 1024;                  // largest activation slab (K <= 1280)
 
 __device__ __forceinline__ void cp_async_16(uint32_t dst, const void *src)
 {
@@ -144,17 +147,30 @@ k1s_gather_kernel(const int32_t *__restrict__ tile_ptr, const uint4 *__restrict_
                   const int4 *__restrict__ tile_idx, int32_t groups, int32_t K, const uint8_t *__restrict__ x,
                   int64_t ldx, int64_t N, void *__restrict__ out, int64_t ldo, EpiParams E)
 {
-    extern __shared__ __align__(16) uint8_t xs[];          // [K][K1_TOK]
+    extern __shared__ __align__(16) uint8_t dyn[];
+    uint4 *ws_w = reinterpret_cast<uint4 *>(dyn);                       // [warp][K1S_TILES] weights
+    int4 *ws_i = reinterpret_cast<int4 *>(dyn + K1S_WBYTES / 2);        // [warp][K1S_TILES] column indices
+    uint8_t *xs = dyn + K1S_WBYTES;                                     // [K][K1_TOK]
     __shared__ uint32_t stage[K1_ROWS][K1_TOK + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int32_t g = blockIdx.y * K1_WARPS + warp;
     const int64_t nb = (int64_t)blockIdx.x * K1_TOK;
     const int64_t n0 = nb + lane * 4;
-    // weights of this warp's first micro-tiles do not depend on the previous kernel
+    // this warp's micro-tiles (weights, column indices) do not depend on the
+    // previous kernel: their copy starts before the grid dependency wait
     int32_t t0 = 0, t1 = 0;
     if (g < groups) {
         t0 = __ldg(tile_ptr + g);
         t1 = __ldg(tile_ptr + g + 1);
+    }
+    const int32_t nst = min(t1 - t0, K1S_TILES);
+    {
+        const uint32_t w_u = (uint32_t)__cvta_generic_to_shared(ws_w + warp * K1S_TILES);
+        const uint32_t i_u = (uint32_t)__cvta_generic_to_shared(ws_i + warp * K1S_TILES);
+        for (int t = lane; t < nst; t += 32) {
+            cp_async_16(w_u + 16 * t, tile_w + t0 + t);
+            cp_async_16(i_u + 16 * t, tile_idx + t0 + t);
+        }
     }
     SI_PDL_ENTRY();
     {
@@ -180,10 +196,13 @@ k1s_gather_kernel(const int32_t *__restrict__ tile_ptr, const uint4 *__restrict_
 
     if (g < groups) {
         const uint32_t *xw = reinterpret_cast<const uint32_t *>(xs) + lane;   // this lane's 4 tokens of row 0
+        const uint4 *sw = ws_w + warp * K1S_TILES;
+        const int4 *si = ws_i + warp * K1S_TILES;
 #pragma unroll 4
-        for (int32_t t = t0; t < t1; ++t) {
-            const uint4 w = __ldg(tile_w + t);
-            const int4 ix = __ldg(tile_idx + t);
+        for (int32_t t = 0; t < t1 - t0; ++t) {
+            // (staged tiles from shared memory, a longer group's tail straight from L2)
+            const uint4 w = t < nst ? sw[t] : __ldg(tile_w + t0 + t);
+            const int4 ix = t < nst ? si[t] : __ldg(tile_idx + t0 + t);
             const uint32_t x0 = xw[ix.x * (K1_TOK / 4)], x1 = xw[ix.y * (K1_TOK / 4)];
             const uint32_t x2 = xw[ix.z * (K1_TOK / 4)], x3 = xw[ix.w * (K1_TOK / 4)];
             const uint32_t lo01 = __byte_perm(x0, x1, 0x5140), lo23 = __byte_perm(x2, x3, 0x5140);
@@ -290,7 +309,7 @@ void launch_k1_mode(const SpmmArgs &a, const uint8_t *x, int64_t ldx, bool vec, 
     auto ti = img_sec<int4>(a.img, h->off_tile_idx);
     // staged variant: 16-byte-aligned [K, N] activations whose slab fits
     const size_t slab = (size_t)h->K * K1_TOK;
-    if (ldx % 16 == 0 && ((uintptr_t)x) % 16 == 0 && slab <= (size_t)K1S_SMEM) {
+    if (ldx % 16 == 0 && ((uintptr_t)x) % 16 == 0 && slab <= (size_t)K1S_SLAB) {
         auto kern = k1s_gather_kernel<MODE, OUTB>;
         static std::mutex mu;
         static std::set<int> done;
@@ -299,9 +318,9 @@ void launch_k1_mode(const SpmmArgs &a, const uint8_t *x, int64_t ldx, bool vec, 
         {
             std::lock_guard<std::mutex> lk(mu);
             if (done.insert(dev).second)
-                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K1S_SMEM);
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K1S_WBYTES + K1S_SLAB);
         }
-        launch_pdl(kern, dim3(grid), dim3(K1_WARPS * 32), slab, st, tp, tw, ti, h->groups, h->K, x, ldx, a.n, a.out,
+        launch_pdl(kern, dim3(grid), dim3(K1_WARPS * 32), K1S_WBYTES + slab, st, tp, tw, ti, h->groups, h->K, x, ldx, a.n, a.out,
                    a.ldo, E);
         return;
     }
@@ -329,6 +348,27 @@ void launch_k1_outb(const SpmmArgs &a, const uint8_t *x, int64_t ldx, bool vec, 
 inline int64_t tpad(int64_t n) { return (n + 15) / 16 * 16; }
 
 }  // namespace
+
+bool k1s_preferred(const SiImage *h, int64_t n, int32_t layout, const void *x, int64_t ldx)
+{
+    // the staged kernel wins where its CTAs fit one wave (one CTA per SM: the
+    // slab takes most of the shared memory) and a group holds few blocks: the
+    // config-2 grid at N = 128 / 512 (profiles/r02c_config2_{gather,tc}.md)
+    // crosses over at ~120 blocks per group (768 @85%, 1024 @90%)
+    if (layout != SI_ACT_KN || ldx % 16 || ((uintptr_t)x) % 16) return false;
+    if ((size_t)h->K * K1_TOK > (size_t)K1S_SLAB) return false;
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        sms = v > 0 ? v : 148;
+    }
+    const int64_t ctas = ((n + K1_TOK - 1) / K1_TOK) * ((h->groups + K1_WARPS - 1) / K1_WARPS);
+    if (ctas > sms) return false;
+    const uint64_t tiles = (h->off_tile_idx - h->off_tile_w) / 16;   // (section padding included: < 64 tiles)
+    return 4 * tiles <= 120ull * (uint64_t)h->groups;
+}
 
 uint64_t k1_workspace(const SiImage *h, int64_t n, int32_t layout)
 {
