@@ -397,3 +397,23 @@ def test_output_into_wider_buffer(kernel, col0):
     got = wide.cpu().numpy()
     check_equal(got[:, col0: col0 + m], oracle.spmm_exec(sw, x, prog, bias), prog, (kernel, col0))
     assert (got[:, :col0] == 0x5A).all() and (got[:, col0 + m:] == 0x5A).all()
+
+
+@pytest.mark.parametrize("m,k,n,ratio,kind", [
+    (256, 1280, 100, 0.0, "gelu_erf_u8"),   # largest staged slab; 320 tiles per group: staged tiles + L2 tail
+    (64, 1296, 48, 0.5, "s32"),             # one row past the slab limit: direct loads
+    (768, 768, 128, 0.9, "deq_f32"),        # BASELINE config 1's shape (the cell AUTO sends to K1s)
+    (36, 1008, 528, 0.9, "requant_u8"),     # ragged tokens over several token tiles
+    (4, 16, 17, 0.0, "s32"),                # one group, one 16-byte chunk
+])
+def test_staged_gather_kernel(m, k, n, ratio, kind):
+    """K1s (spmm_gather.cu): the gather kernel with the activation slab and
+    each warp's micro-tiles staged in shared memory by cp.async, against the
+    oracle, through kernel="gather" and through AUTO, both layouts."""
+    w, x, bias, scales = baseline_inputs(m, k, n, ratio, 4321 + m + k)
+    sw = P.encode_sparse(w, scales)
+    prog = workloads.program(kind, scales, a_zp=3)
+    want = oracle.spmm_exec(sw, x, prog, bias)
+    for kernel in ("gather", "auto"):
+        for layout in ("kn", "nk"):
+            check_equal(run(sw, x, prog, bias, kernel=kernel, layout=layout), want, prog, (m, k, n, kernel, layout))
