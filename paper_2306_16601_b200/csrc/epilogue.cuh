@@ -232,8 +232,12 @@ __device__ __forceinline__ int32_t bp_lookup_linear(float x, const uint2 *tab, f
     t = fminf(fmaxf(t, 0.0f), nbm1);
     const uint32_t b = __float_as_uint(__fadd_rn(t, 8388608.0f)) & 0x7FFFFFu;
     const uint2 e = tab[b];
-    const int32_t w = (int32_t)e.y;
-    return x >= __uint_as_float(e.x) ? (w >> 16) : ((w << 16) >> 16);
+    // sign-extended 16-bit half of e.y picked by one PRMT (selector nibble msb:
+    // replicate the byte's sign): 0xBB32 = upper half, 0x9910 = lower half
+    const uint32_t sel = x >= __uint_as_float(e.x) ? 0xBB32u : 0x9910u;
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %1, %2;" : "=r"(r) : "r"(e.y), "r"(sel));
+    return (int32_t)r;
 }
 
 // _run_chain interpreter (epilogue.py:207-249) for EPI_GENERIC

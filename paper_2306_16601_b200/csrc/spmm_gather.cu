@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <mutex>
 #include <set>
 
@@ -357,12 +358,14 @@ bool k1s_preferred(const SiImage *h, int64_t n, int32_t layout, const void *x, i
     // crosses over at ~120 blocks per group (768 @85%, 1024 @90%)
     if (layout != SI_ACT_KN || ldx % 16 || ((uintptr_t)x) % 16) return false;
     if ((size_t)h->K * K1_TOK > (size_t)K1S_SLAB) return false;
-    static int sms = 0;
+    static std::atomic<int> sm_count{0};   // (every GPU of a node is the same part)
+    int sms = sm_count.load(std::memory_order_relaxed);
     if (sms == 0) {
         int dev = 0, v = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
         sms = v > 0 ? v : 148;
+        sm_count.store(sms, std::memory_order_relaxed);
     }
     const int64_t ctas = ((n + K1_TOK - 1) / K1_TOK) * ((h->groups + K1_WARPS - 1) / K1_WARPS);
     if (ctas > sms) return false;
