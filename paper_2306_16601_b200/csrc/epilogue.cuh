@@ -240,6 +240,23 @@ __device__ __forceinline__ int32_t bp_lookup_linear(float x, const uint2 *tab, f
     return (int32_t)r;
 }
 
+// The same lookup for a table staged in shared memory.  `biased` is the
+// table's 32-bit shared address minus (0x4B000000 << 3): the float bits of
+// t + 2^23 are 0x4B000000 + b, so (bits << 3) + biased wraps to the address of
+// entry b in one shift-add (no mask, no separate base add).
+__device__ __forceinline__ int32_t bp_lookup_linear_smem(float x, uint32_t biased, float inv, float off, float nbm1)
+{
+    float t = __fmaf_rn(x, inv, off);
+    t = fminf(fmaxf(t, 0.0f), nbm1);
+    const uint32_t addr = (__float_as_uint(__fadd_rn(t, 8388608.0f)) << 3) + biased;
+    uint32_t ex, ey;
+    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(ex), "=r"(ey) : "r"(addr));
+    const uint32_t sel = x >= __uint_as_float(ex) ? 0xBB32u : 0x9910u;
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %1, %2;" : "=r"(r) : "r"(ey), "r"(sel));
+    return (int32_t)r;
+}
+
 // _run_chain interpreter (epilogue.py:207-249) for EPI_GENERIC
 static __device__ __noinline__ uint32_t epi_generic(int32_t acc, int32_t m, int64_t n, const EpiParams &E)
 {

@@ -245,10 +245,10 @@ __device__ __forceinline__ void epi_chunk(uint32_t taddr, int32_t m, bool mok, i
         }
         if (E.bp_lin_n > 0) {
             // (uniform) linear buckets with one threshold each: one compare
-            const uint2 *lin = reinterpret_cast<const uint2 *>(W.s_key);
+            const uint32_t lin = tc::smem_u32(W.s_key) - (0x4B000000u << 3);
             const float nbm1 = (float)(E.bp_lin_n - 1);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = bp_lookup_linear(x[j], lin, E.bp_lin_inv, E.bp_lin_off, nbm1);
+            for (int j = 0; j < 32; ++j) v[j] = bp_lookup_linear_smem(x[j], lin, E.bp_lin_inv, E.bp_lin_off, nbm1);
         } else
         // (uniform branch on the plan's bucket occupancy) fixed-step lookups
 #define SI_BP_CHUNK(S)                                                                                          \
